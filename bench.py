@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: device-timed forward + backprojection images/s on the B200
+kernels (BASELINE.json metric, configs[1]: parallel-beam 512x512, 512 angles,
+512 detectors, batch 128, fp32), sharded across N GPUs with no collective on
+the data path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload par512|fan512|fbp1024]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+One step = forward(images) -> sinogram, then backprojection(sinogram) ->
+images, over this rank's contiguous shard of the global batch.  Inputs are
+resident in HBM when the timed region starts; the L2 is flushed (a 256 MiB
+write) between timed steps, outside the timed events.  Per-kernel device time
+comes from the library's own event instrumentation (rk_profiling_*), the
+roofline peak from the library's shared-memory bandwidth probe, and the
+end-to-end number from the reference-shaped host-buffer entry points
+(rk_forward_host / rk_backproject_host: pinned host in, host out, copies in
+the timed region).  The CPU baseline is the reference itself compiled in
+place (oracle/_ref), timed on this host's cores on a bounded sample.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+GLOBAL_BATCH = 128
+METRIC = "forward+back-projection images/s (512², 512 angles, batch 128) at 1/2/4/8 GPUs"
+
+WORKLOADS = {
+    # name: (kind, size, n_angles, angle_stop, det_count, source_distance, global batch)
+    "par512": ("parallel", 512, 512, math.pi, 512, 0.0, 128),
+    "fan512": ("fanbeam", 512, 512, 2 * math.pi, 512, 512.0, 128),
+}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def shard(batch, world, rank):
+    """Contiguous shard of ceil(batch / world) elements."""
+    per = -(-batch // world)
+    lo = min(batch, rank * per)
+    return lo, min(batch, lo + per)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_images_per_s(wl, budget_s=12.0, warmup=1, fixed_batch=None):
+    """The reference (oracle/_ref: radonkit compiled in place) forward + backprojection
+    on this host's cores, all threads, on a bounded sample of the workload."""
+    from oracle import Geom, RefOracle, default_oracle
+
+    try:
+        orc = RefOracle()
+        kind = "reference"
+    except (FileNotFoundError, OSError):
+        orc = default_oracle()
+        kind = "port"
+    cores = os.cpu_count() or 1
+    if kind == "reference":
+        orc.set_num_threads(cores)
+    k, s, na, stop, nd, src, _ = WORKLOADS[wl]
+    g = Geom(k, s, orc.angles_linspace(0.0, stop, na), nd, None, src)
+    ph = orc.shepp_logan(s)
+
+    def run(b):
+        x = np.repeat(ph, b, axis=0)
+        t0 = time.perf_counter()
+        y = orc.forward(g, x)
+        orc.backprojection(g, y)
+        return time.perf_counter() - t0
+
+    t1 = run(1)  # also the warm-up
+    for _ in range(max(0, warmup - 1)):
+        run(1)
+    b = fixed_batch or max(1, min(64, int(budget_s / 3.0 / max(t1, 1e-3))))
+    times = [run(b) for _ in range(3)]
+    med = statistics.median(times)
+    return {"value": b / med, "unit": "images/s", "cores": cores, "kind": kind,
+            "sample": f"{b} x {s}^2 image(s), {na} angles, {nd} cells per run; median of 3 runs after 1 warm-up; "
+                      f"{'parallel' if k == 'parallel' else 'fan-beam'}; set_num_threads({cores})"}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation on the host cores."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    from oracle import Geom, RefOracle, default_oracle
+
+    try:
+        orc = RefOracle()
+        kind = "reference"
+    except (FileNotFoundError, OSError):
+        orc = default_oracle()
+        kind = "port"
+    cores = os.cpu_count() or 1
+    if kind == "reference":
+        orc.set_num_threads(cores)
+    k, s, na, stop, nd, src, B = WORKLOADS[args.workload]
+    g = Geom(k, s, orc.angles_linspace(0.0, stop, na), nd, None, src)
+    ph = orc.shepp_logan(s)
+    x1 = ph.copy()
+    t0 = time.perf_counter()
+    orc.backprojection(g, orc.forward(g, x1))
+    t1 = time.perf_counter() - t0
+    per_step = max(1, min(B, int(6.0 / max(t1, 1e-3))))  # bounded sample: ~6 s of CPU work per step
+    x = np.repeat(ph, per_step, axis=0)
+    for _ in range(args.warmup):
+        orc.backprojection(g, orc.forward(g, x[:1]))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.backprojection(g, orc.forward(g, x))
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = per_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32 storage, fp64 accumulate",
+        "data": "synthetic: modified Shepp-Logan phantom (reference shepp_logan)",
+        "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
+                   "sample_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} image(s) per step of the {args.workload} workload"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="par512", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    import paper_2009_14788_b200 as rk
+    from paper_2009_14788_b200 import _lib
+    from oracle import batched_phantom  # noqa: F401  (input generator only)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    k, s, na, stop, nd, src, B = WORKLOADS[args.workload]
+    ang = rk.angles_linspace(0.0, stop, na)
+    g = rk.make_parallel(s, ang, nd) if k == "parallel" else rk.make_fanbeam(s, ang, src, det_count=nd)
+    lo, hi = shard(B, world, rank)
+    nb = hi - lo
+
+    # synthetic inputs: phantom x (e+1)/128, Rng(seed=e) uniform for odd e
+    ph = rk_phantom(s)
+    imgs = np.empty((nb, s, s), np.float32)
+    for i, e in enumerate(range(lo, hi)):
+        if e % 2 == 0:
+            imgs[i] = ph * np.float32((e + 1) / 128.0)
+        else:
+            imgs[i] = rk.Rng(e).uniform_tensor((s, s))
+    x = torch.from_numpy(imgs).to(dev)
+    sino = torch.empty(nb, na, nd, device=dev)
+    out = torch.empty(nb, s, s, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    plan = rk.get_plan(g, None, local)
+    info = plan.info()
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes_void(stream.cuda_stream)
+
+    def step():
+        _lib.check(_lib.lib.rk_forward(plan.handle, _lib.RK_F32, ctypes_void(x.data_ptr()), nb,
+                                       ctypes_void(sino.data_ptr()), sp))
+        _lib.check(_lib.lib.rk_backproject(plan.handle, _lib.RK_F32, ctypes_void(sino.data_ptr()), nb,
+                                           ctypes_void(out.data_ptr()), sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    smem_peak = ctypes_double()
+    _lib.check(_lib.lib.rk_probe_smem_bandwidth(local, smem_peak))
+    stats = _lib.RkKernelStats()
+    _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    _lib.check(_lib.lib.rk_profiling_enable(1))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush between timed steps (outside the events)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    _lib.check(_lib.lib.rk_profiling_enable(0))
+    _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = B / (ms_per_step * 1e-3)
+
+    kinds = _lib.KERNEL_KINDS
+    launches = int(sum(stats.launches[i] for i in range(len(kinds))))
+    kern = {kinds[i]: {"launches": int(stats.launches[i]), "ms_total": float(stats.ms[i]),
+                       "ms_per_launch": (float(stats.ms[i]) / stats.timed[i]) if stats.timed[i] else None}
+            for i in range(len(kinds)) if stats.launches[i]}
+    # roofline of the dominant kernel: algorithmic L1TEX/SMEM bytes per launch
+    # (16 B per forward sample = 4 fp32 taps; 8 B per backprojection sample = 2 taps)
+    fwd_bytes = 16.0 * info["forward_samples"] * nb
+    bp_bytes = 8.0 * info["backproject_samples"] * nb
+    fwd_ms = kern.get("forward", {}).get("ms_per_launch") or float("nan")
+    bp_ms = kern.get("backproject", {}).get("ms_per_launch") or float("nan")
+    dom, dbytes, dms = ("forward", fwd_bytes, fwd_ms) if fwd_ms >= bp_ms else ("backproject", bp_bytes, bp_ms)
+    achieved = dbytes / (dms * 1e-3) / 1e9
+    peak = float(smem_peak.value)
+    roofline = {"bound": "l1tex", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "measured in this run by rk_probe_smem_bandwidth (LDS.128, all SMs); "
+                               "MEASURED_PEAKS.json has no L1TEX/SMEM figure",
+                "algorithmic_bytes_per_launch": dbytes,
+                "per_kernel": {
+                    "forward": {"samples_per_launch": info["forward_samples"] * nb, "bytes_per_sample": 16,
+                                "ms": fwd_ms, "gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9,
+                                "gsamples_per_s": info["forward_samples"] * nb / (fwd_ms * 1e-3) / 1e9},
+                    "backproject": {"samples_per_launch": info["backproject_samples"] * nb, "bytes_per_sample": 8,
+                                    "ms": bp_ms, "gbs": bp_bytes / (bp_ms * 1e-3) / 1e9,
+                                    "gsamples_per_s": info["backproject_samples"] * nb / (bp_ms * 1e-3) / 1e9}}}
+
+    # ---- end to end through the reference-shaped host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        h_img = torch.from_numpy(imgs).pin_memory()
+        h_sino = torch.empty(nb, na, nd).pin_memory()
+        h_out = torch.empty(nb, s, s).pin_memory()
+
+        def e2e_step():
+            _lib.check(_lib.lib.rk_forward_host(plan.handle, _lib.RK_F32, ctypes_void(h_img.data_ptr()), nb,
+                                                ctypes_void(h_sino.data_ptr())))
+            _lib.check(_lib.lib.rk_backproject_host(plan.handle, _lib.RK_F32, ctypes_void(h_sino.data_ptr()), nb,
+                                                    ctypes_void(h_out.data_ptr())))
+
+        for _ in range(2):
+            e2e_step()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        bi = 4 * nb * (s * s + na * nd)
+        e2e = {"value": B * args.steps / el, "unit": "images/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi,
+               "ms_per_step": 1e3 * el / args.steps,
+               "path": "rk_forward_host + rk_backproject_host (pinned host buffers, 2-stream chunked copy/compute "
+                       "pipeline, synchronous like the reference's Tensor-in/Tensor-out calls)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_images_per_s(args.workload)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic: modified Shepp-Logan phantom x (e+1)/128 for even e, Rng(e) uniform for odd e",
+            "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
+                       "global_batch": B, "per_gpu_batch": nb, "parallelism": f"batch-shard x{world}, no collective",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kern,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def rk_phantom(s):
+    """Modified Shepp-Logan via the oracle port (input generation only, not timed)."""
+    from oracle import PortOracle
+
+    return PortOracle().shepp_logan(s)[0]
+
+
+def ctypes_void(p):
+    import ctypes
+
+    return ctypes.c_void_p(p)
+
+
+def ctypes_double():
+    import ctypes
+
+    return ctypes.c_double()
+
+
+def ctypes_ref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,415 @@
+// extern "C" boundary of the B200 Radon projector (include/radon_b200.h).
+// Each entry point validates like the reference function it replaces
+// (cited), enqueues the CUDA work and maps exceptions onto rk_status codes.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include "rk_internal.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RK_OK;
+  } catch (const rk::ValidationError& e) {
+    g_last_error = e.what();
+    return RK_ERR_VALIDATION;
+  } catch (const rk::NumericalError& e) {
+    g_last_error = e.what();
+    return RK_ERR_NUMERICAL;
+  } catch (const rk::CudaError& e) {
+    g_last_error = e.what();
+    return RK_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RK_ERR_CUDA;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw rk::ValidationError(msg);
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// The plan's scratch is shared by every call on the plan: serialise host
+// enqueue with the mutex and order device reuse across streams with an event.
+struct ScratchLease {
+  rk::Plan& p;
+  cudaStream_t st;
+  std::lock_guard<std::mutex> lock;
+  ScratchLease(rk::Plan& plan, cudaStream_t stream) : p(plan), st(stream), lock(plan.mu) {
+    RK_CUDA(cudaSetDevice(p.device));
+    RK_CUDA(cudaStreamWaitEvent(st, p.scratch_free, 0));
+  }
+  ~ScratchLease() { cudaEventRecord(p.scratch_free, st); }
+};
+
+size_t packed_image_bytes(const rk::Plan& p, int64_t batch) {
+  return size_t(rk::groups_of(batch)) * size_t(p.s + 2) * size_t(p.s + 2) * sizeof(float4);
+}
+size_t packed_sino_bytes(const rk::Plan& p, int64_t batch) {
+  return size_t(rk::groups_of(batch)) * size_t(p.na) * size_t(p.nd) * sizeof(float4);
+}
+
+void check_plan(const rk_plan* plan) { require(plan != nullptr, "plan is null"); }
+
+void check_device_plan(const rk_plan* plan) {
+  check_plan(plan);
+  require(plan->p.device >= 0, "plan was created host-only (device -1); it cannot run kernels");
+}
+
+void check_device_filter(const rk_filter* f) {
+  require(f != nullptr, "filter is null");
+  require(f->f.device >= 0, "filter was created host-only (device -1); it cannot run kernels");
+}
+
+// Device-pointer bodies, reused by the host-buffer pipelines with their own scratch.
+void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
+                  cudaStream_t st) {
+  pk.reserve(packed_image_bytes(p, batch));
+  rk::launch_pack_images(dtype, d_image, batch, p.s, pk.as<float4>(), st);
+  rk::launch_forward(p, pk.as<float4>(), batch, dtype, d_sino, st);
+}
+
+void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
+                      rk::DeviceBuffer& pk, cudaStream_t st) {
+  pk.reserve(packed_sino_bytes(p, batch));
+  rk::launch_pack_sino(dtype, d_sino, batch, p.na, p.nd, pk.as<float4>(), st);
+  rk::launch_backproject(p, pk.as<float4>(), batch, dtype, d_image, st);
+}
+
+void fbp_into(rk::Plan& p, rk::Filter& f, int dtype, const void* d_sino, int64_t batch, void* d_image,
+              rk::DeviceBuffer& pk, cudaStream_t st) {
+  pk.reserve(packed_sino_bytes(p, batch));
+  // the filter writes straight into the packed layout the backprojector reads
+  rk::launch_filter(f, dtype, d_sino, batch, p.na, nullptr, pk.as<float4>(), st);
+  rk::launch_backproject(p, pk.as<float4>(), batch, dtype, d_image, st);
+}
+
+void check_dtype(int dtype) { (void)rk::dtype_size(dtype); }
+
+// ------------------------------------------------------------------ host pipelines
+// Reference-shaped calls (host Tensor in, host Tensor out): the batch is cut
+// into chunks of whole packed groups, and chunk i+1's host->device copy, chunk
+// i's kernels and chunk i-1's device->host copy overlap on two streams.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
+template <class Body>
+void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_item, const void* h_in, void* h_out,
+                       Body body) {
+  std::lock_guard<std::mutex> lock(p.mu);
+  RK_CUDA(cudaSetDevice(p.device));
+  for (auto& s : p.copy_streams)
+    if (!s) RK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // host calls are synchronous: wait for any device-pointer call still using scratch
+  RK_CUDA(cudaEventSynchronize(p.scratch_free));
+  // ~8 chunks, each a whole number of packed groups and >= 4 MB of input
+  int64_t chunk = std::max<int64_t>(rk::kPack, (batch + 7) / 8);
+  chunk = (chunk + rk::kPack - 1) / rk::kPack * rk::kPack;
+  int64_t min_items = std::max<int64_t>(1, int64_t((4u << 20) / std::max<size_t>(in_item, 1)));
+  min_items = (min_items + rk::kPack - 1) / rk::kPack * rk::kPack;
+  chunk = std::min(batch, std::max(chunk, min_items));
+  const bool pinned_in = is_pinned(h_in), pinned_out = is_pinned(h_out);
+  for (int i = 0; i < 2; ++i) {
+    p.pipe_in[i].reserve(size_t(chunk) * in_item);
+    p.pipe_out[i].reserve(size_t(chunk) * out_item);
+  }
+  int slot = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, slot ^= 1) {
+    const int64_t nb = std::min(chunk, batch - b0);
+    cudaStream_t st = p.copy_streams[slot];
+    const char* src = static_cast<const char*>(h_in) + size_t(b0) * in_item;
+    char* dst = static_cast<char*>(h_out) + size_t(b0) * out_item;
+    RK_CUDA(cudaMemcpyAsync(p.pipe_in[slot].ptr, src, size_t(nb) * in_item, cudaMemcpyHostToDevice, st));
+    body(p.pipe_in[slot].ptr, nb, p.pipe_out[slot].ptr, p.pipe_pk[slot], st);
+    RK_CUDA(cudaMemcpyAsync(dst, p.pipe_out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
+    if (!pinned_in || !pinned_out) RK_CUDA(cudaStreamSynchronize(st));
+  }
+  for (auto s : p.copy_streams) RK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rk_last_error(void) { return g_last_error.c_str(); }
+
+const char* rk_version(void) { return "radon_b200 0.1 (sm_100a)"; }
+
+int rk_geometry_resolve(const rk_geometry* in, rk_geometry* out) {
+  return guarded([&] {
+    require(in != nullptr && out != nullptr, "geometry pointer is null");
+    *out = rk::resolve_geometry(*in);
+  });
+}
+
+int rk_angles_linspace(double start, double stop, int64_t n, double* out) {
+  return guarded([&] {  // geometry.cpp:67-73
+    if (n < 1) throw rk::ValidationError("angle count must be >= 1, got " + std::to_string(n));
+    require(out != nullptr, "output pointer is null");
+    double step = (stop - start) / double(n);
+    for (int64_t i = 0; i < n; ++i) out[i] = start + double(i) * step;
+  });
+}
+
+int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan) {
+  return guarded([&] {
+    require(geometry != nullptr && plan != nullptr, "geometry / plan pointer is null");
+    *plan = nullptr;
+    auto hp = std::make_unique<rk_plan>();
+    rk::Plan& p = hp->p;
+    p.device = device;
+    p.angles.assign(geometry->angles, geometry->angles + std::max<int64_t>(geometry->n_angles, 0));
+    rk_geometry in = *geometry;
+    in.angles = p.angles.data();
+    p.g = rk::resolve_geometry(in);
+    p.g.angles = p.angles.data();
+    if (device >= 0) {
+      int count = 0;
+      RK_CUDA(cudaGetDeviceCount(&count));
+      require(device < count, "device " + std::to_string(device) + " out of range");
+    }
+    rk::build_plan(p);
+    *plan = hp.release();
+  });
+}
+
+int rk_plan_destroy(rk_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    cudaSetDevice(plan->p.device);
+    cudaDeviceSynchronize();
+    delete plan;
+  });
+}
+
+int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info) {
+  return guarded([&] {
+    check_plan(plan);
+    require(info != nullptr, "info pointer is null");
+    const rk::Plan& p = plan->p;
+    info->geometry = p.g;
+    info->forward_samples = p.forward_samples;
+    info->backproject_samples = p.s * p.s * p.na;
+    info->device = p.device;
+    info->reserved = 0;
+  });
+}
+
+// projector.cpp:228-236 (forward: shape + options checked, output keeps the precision)
+int rk_forward(rk_plan* plan, int dtype, const void* d_image, int64_t batch, void* d_sino, void* stream) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_image != nullptr && d_sino != nullptr, "image / sinogram pointer is null");
+    rk::Plan& p = plan->p;
+    ScratchLease lease(p, as_stream(stream));
+    forward_into(p, dtype, d_image, batch, d_sino, p.packed_image, as_stream(stream));
+  });
+}
+
+// projector.cpp:252-260
+int rk_backproject(rk_plan* plan, int dtype, const void* d_sino, int64_t batch, void* d_image, void* stream) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_image != nullptr && d_sino != nullptr, "image / sinogram pointer is null");
+    rk::Plan& p = plan->p;
+    ScratchLease lease(p, as_stream(stream));
+    backproject_into(p, dtype, d_sino, batch, d_image, p.packed_sino, as_stream(stream));
+  });
+}
+
+int rk_filter_kind_from_name(const char* name, int* kind) {
+  return guarded([&] {
+    require(name != nullptr && kind != nullptr, "name / kind pointer is null");
+    *kind = rk::filter_kind_from_name(name);
+  });
+}
+
+const char* rk_filter_kind_name(int kind) { return rk::filter_kind_name(kind); }
+
+int rk_filter_create(int kind, int64_t det_count, int device, rk_filter** filter) {
+  return guarded([&] {
+    require(filter != nullptr, "filter pointer is null");
+    *filter = nullptr;
+    auto hf = std::make_unique<rk_filter>();
+    hf->f.device = device;
+    if (device >= 0) {
+      int count = 0;
+      RK_CUDA(cudaGetDeviceCount(&count));
+      require(device < count, "device " + std::to_string(device) + " out of range");
+    }
+    rk::build_filter(hf->f, kind, det_count);
+    *filter = hf.release();
+  });
+}
+
+int rk_filter_destroy(rk_filter* filter) {
+  return guarded([&] {
+    if (!filter) return;
+    cudaSetDevice(filter->f.device);
+    cudaDeviceSynchronize();
+    delete filter;
+  });
+}
+
+int rk_filter_response(const rk_filter* filter, int64_t* padded_size, double* response, float* response_f) {
+  return guarded([&] {
+    require(filter != nullptr, "filter is null");
+    const rk::Filter& f = filter->f;
+    if (padded_size) *padded_size = f.padded;
+    if (response) std::memcpy(response, f.response.data(), f.response.size() * sizeof(double));
+    if (response_f) std::memcpy(response_f, f.response_f.data(), f.response_f.size() * sizeof(float));
+  });
+}
+
+// sino_filter.cpp:98-104 (3-D shape, det_count must match the filter)
+int rk_filter_sinogram(rk_filter* filter, int dtype, const void* d_in, int64_t batch, int64_t n_angles,
+                       void* d_out, void* stream) {
+  return guarded([&] {
+    check_device_filter(filter);
+    check_dtype(dtype);
+    require(batch >= 1 && n_angles >= 1, "sinogram must have batch >= 1 and n_angles >= 1");
+    require(d_in != nullptr && d_out != nullptr, "sinogram pointer is null");
+    rk::Filter& f = filter->f;
+    std::lock_guard<std::mutex> lock(f.mu);
+    RK_CUDA(cudaSetDevice(f.device));
+    rk::launch_filter(f, dtype, d_in, batch, n_angles, d_out, nullptr, as_stream(stream));
+  });
+}
+
+// sino_filter.cpp:126-136
+int rk_fbp(rk_plan* plan, rk_filter* filter, int dtype, const void* d_sino, int64_t batch, void* d_image,
+           void* stream) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_device_filter(filter);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_sino != nullptr && d_image != nullptr, "sinogram / image pointer is null");
+    rk::Plan& p = plan->p;
+    require(filter->f.det_count == p.nd, "sinogram det_count " + std::to_string(p.nd) +
+                                             " does not match filter " + std::to_string(filter->f.det_count));
+    require(filter->f.device == p.device, "filter and plan live on different devices");
+    ScratchLease lease(p, as_stream(stream));
+    fbp_into(p, filter->f, dtype, d_sino, batch, d_image, p.packed_sino, as_stream(stream));
+  });
+}
+
+int rk_forward_host(rk_plan* plan, int dtype, const void* h_image, int64_t batch, void* h_sino) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(h_image != nullptr && h_sino != nullptr, "image / sinogram pointer is null");
+    rk::Plan& p = plan->p;
+    const size_t es = rk::dtype_size(dtype);
+    run_host_pipeline(p, batch, size_t(p.s * p.s) * es, size_t(p.na * p.nd) * es, h_image, h_sino,
+                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
+                        forward_into(p, dtype, din, nb, dout, pk, st);
+                      });
+  });
+}
+
+int rk_backproject_host(rk_plan* plan, int dtype, const void* h_sino, int64_t batch, void* h_image) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(h_image != nullptr && h_sino != nullptr, "image / sinogram pointer is null");
+    rk::Plan& p = plan->p;
+    const size_t es = rk::dtype_size(dtype);
+    run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
+                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
+                        backproject_into(p, dtype, din, nb, dout, pk, st);
+                      });
+  });
+}
+
+int rk_filter_sinogram_host(rk_filter* filter, int dtype, const void* h_in, int64_t batch, int64_t n_angles,
+                            void* h_out) {
+  return guarded([&] {
+    check_device_filter(filter);
+    check_dtype(dtype);
+    require(batch >= 1 && n_angles >= 1, "sinogram must have batch >= 1 and n_angles >= 1");
+    require(h_in != nullptr && h_out != nullptr, "sinogram pointer is null");
+    rk::Filter& f = filter->f;
+    std::lock_guard<std::mutex> lock(f.mu);
+    RK_CUDA(cudaSetDevice(f.device));
+    const size_t bytes = size_t(batch * n_angles * f.det_count) * rk::dtype_size(dtype);
+    rk::DeviceBuffer din, dout;
+    din.reserve(bytes);
+    dout.reserve(bytes);
+    RK_CUDA(cudaMemcpy(din.ptr, h_in, bytes, cudaMemcpyHostToDevice));
+    rk::launch_filter(f, dtype, din.ptr, batch, n_angles, dout.ptr, nullptr, nullptr);
+    RK_CUDA(cudaMemcpy(h_out, dout.ptr, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino, int64_t batch, void* h_image) {
+  return guarded([&] {
+    check_device_plan(plan);
+    check_device_filter(filter);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(h_image != nullptr && h_sino != nullptr, "image / sinogram pointer is null");
+    rk::Plan& p = plan->p;
+    require(filter->f.det_count == p.nd, "sinogram det_count " + std::to_string(p.nd) +
+                                             " does not match filter " + std::to_string(filter->f.det_count));
+    const size_t es = rk::dtype_size(dtype);
+    run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
+                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
+                        fbp_into(p, filter->f, dtype, din, nb, dout, pk, st);
+                      });
+  });
+}
+
+int rk_estimate_alpha(rk_plan* plan, int iterations, uint64_t seed, double* alpha) {
+  return guarded([&] { throw rk::ValidationError("rk_estimate_alpha: not built yet"); });
+}
+
+int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, double alpha,
+                 int iterations, void* d_x, int* failed_iteration, void* stream) {
+  return guarded([&] { throw rk::ValidationError("rk_landweber: not built yet"); });
+}
+
+int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter,
+            double tolerance, void* d_x, int* failed_iteration, void* stream) {
+  return guarded([&] { throw rk::ValidationError("rk_cgne: not built yet"); });
+}
+
+int rk_profiling_enable(int enable) {
+  return guarded([&] { rk::profiling_enable(enable != 0); });
+}
+
+int rk_profiling_read(rk_kernel_stats* stats, int reset) {
+  return guarded([&] {
+    require(stats != nullptr, "stats pointer is null");
+    rk::profiling_read(stats, reset != 0);
+  });
+}
+
+int rk_probe_smem_bandwidth(int device, double* gbs) {
+  return guarded([&] {
+    require(gbs != nullptr, "output pointer is null");
+    *gbs = rk::probe_smem_bandwidth(device);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,357 @@
+// Host side of the B200 Radon projector: geometry resolution/validation, the
+// fp64 per-ray and per-angle tables the kernels consume, and the ramp filter
+// response.  Compiled with -ffp-contract=off so every fp64 expression below
+// is evaluated exactly as written — the same expressions, in the same order,
+// as the reference (cited per function), which keeps the discontinuous
+// sample count n = max(1, ceil(len/step)) identical on every ray (SURVEY
+// appendix A.2).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <limits>
+
+#include "rk_internal.hpp"
+
+namespace rk {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DeviceBuffer::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+void DeviceBuffer::reserve(size_t n) {
+  if (n <= bytes) return;
+  release();
+  RK_CUDA(cudaMalloc(&ptr, n));
+  bytes = n;
+}
+
+Plan::~Plan() {
+  if (scratch_free) cudaEventDestroy(scratch_free);
+  for (auto& s : copy_streams)
+    if (s) cudaStreamDestroy(s);
+}
+
+size_t dtype_size(int dtype) {
+  switch (dtype) {
+    case RK_F16: return 2;
+    case RK_F32: return 4;
+    case RK_F64: return 8;
+  }
+  throw ValidationError("unknown dtype " + std::to_string(dtype) + " (expected RK_F16, RK_F32 or RK_F64)");
+}
+
+// ----------------------------------------------------------------- geometry
+// geometry.cpp:12-19 (check_common), :22-33 (make_parallel), :35-55 (make_fanbeam)
+rk_geometry resolve_geometry(const rk_geometry& in) {
+  if (in.image_size < 1) throw ValidationError("image_size must be >= 1, got " + std::to_string(in.image_size));
+  if (in.n_angles < 1 || in.angles == nullptr) throw ValidationError("angle list must not be empty");
+  for (int64_t a = 0; a < in.n_angles; ++a)
+    if (!std::isfinite(in.angles[a])) throw ValidationError("angles must be finite");
+  rk_geometry g = in;
+  g.has = RK_HAS_DET_COUNT | RK_HAS_DET_SPACING | RK_HAS_DET_DISTANCE;
+  g.det_count = (in.has & RK_HAS_DET_COUNT) ? in.det_count : in.image_size;
+  if (in.kind == RK_PARALLEL) {
+    g.det_spacing = (in.has & RK_HAS_DET_SPACING) ? in.det_spacing : 1.0;
+    if (g.det_count < 1) throw ValidationError("det_count must be >= 1, got " + std::to_string(g.det_count));
+    if (!(g.det_spacing > 0.0)) throw ValidationError("det_spacing must be positive");
+    g.source_distance = 0.0;
+    g.det_distance = 0.0;
+  } else if (in.kind == RK_FANBEAM) {
+    double rmin = double(in.image_size) * std::sqrt(2.0) / 2.0;
+    if (!(in.source_distance > rmin))
+      throw ValidationError("source_distance " + std::to_string(in.source_distance) +
+                            " must exceed image_size/sqrt(2) = " + std::to_string(rmin) +
+                            " so the source stays outside the image");
+    g.det_distance = (in.has & RK_HAS_DET_DISTANCE) ? in.det_distance : in.source_distance;
+    if (!(g.det_distance > 0.0)) throw ValidationError("det_distance must be positive");
+    if (g.det_count < 1) throw ValidationError("det_count must be >= 1, got " + std::to_string(g.det_count));
+    double magnification = (g.source_distance + g.det_distance) / g.source_distance;
+    g.det_spacing = (in.has & RK_HAS_DET_SPACING) ? in.det_spacing
+                                                  : magnification * double(in.image_size) / double(g.det_count);
+    if (!(g.det_spacing > 0.0)) throw ValidationError("det_spacing must be positive");
+  } else {
+    throw ValidationError("unknown geometry kind " + std::to_string(in.kind));
+  }
+  return g;
+}
+
+namespace {
+
+// projector.cpp:37-45
+inline bool clip_slab(double o, double d, double lo, double hi, double& t0, double& t1) {
+  if (d == 0.0) return o >= lo && o <= hi;
+  double a = (lo - o) / d;
+  double b = (hi - o) / d;
+  if (a > b) std::swap(a, b);
+  t0 = std::max(t0, a);
+  t1 = std::min(t1, b);
+  return true;
+}
+
+struct RaySetup {
+  float4 geom;  // px0, py0, hx, hy (padded pixel coordinates)
+  float2 len;   // h, n
+  int64_t n;
+};
+
+// The clip / sample-count / spacing prologue of integrate_ray
+// (projector.cpp:66-78), followed by the change of variables into padded
+// pixel coordinates used by bilinear (projector.cpp:48-49):
+//   px(m) = x(t_m) + s/2 - 0.5 (+1 border) = px0 + (m + 0.5) * hx
+//   py(m) = s/2 - y(t_m) - 0.5 (+1 border) = py0 + (m + 0.5) * hy
+// with t_m = t0 + (m + 0.5) * h.
+RaySetup setup_ray(int64_t s, double ox, double oy, double dx, double dy, double tmin, double tmax, double step) {
+  RaySetup r{};
+  double half = 0.5 * double(s);
+  double t0 = tmin, t1 = tmax;
+  bool hit = clip_slab(ox, dx, -half, half, t0, t1) && clip_slab(oy, dy, -half, half, t0, t1) && (t1 > t0);
+  if (!hit) {
+    r.geom = make_float4(0.f, 0.f, 0.f, 0.f);
+    int zero = 0;
+    float zf;
+    std::memcpy(&zf, &zero, 4);
+    r.len = make_float2(0.f, zf);
+    r.n = 0;
+    return r;
+  }
+  double len = t1 - t0;
+  int64_t n = std::max<int64_t>(1, int64_t(std::ceil(len / step)));
+  double h = len / double(n);
+  double ex = ox + t0 * dx, ey = oy + t0 * dy;  // clipped entry point
+  double px0 = ex + half + 0.5;                 // x + s/2 - 0.5, +1 border
+  double py0 = half - ey + 0.5;                 // s/2 - y - 0.5, +1 border
+  r.geom = make_float4(float(px0), float(py0), float(h * dx), float(-(h * dy)));
+  int ni = int(n);
+  float nf;
+  std::memcpy(&nf, &ni, 4);
+  r.len = make_float2(float(h), nf);
+  r.n = n;
+  return r;
+}
+
+}  // namespace
+
+// Tile geometry of the backprojection kernel (kernels.cu): 32 x 32 pixels.
+constexpr int kBpTile = 32;
+
+void build_plan(Plan& p) {
+  const rk_geometry& g = p.g;
+  p.s = g.image_size;
+  p.na = g.n_angles;
+  p.nd = g.det_count;
+  if (!(g.step > 0.0)) throw ValidationError("projector step must be positive");  // projector.cpp:31-33
+  if (p.s > 32768) throw ValidationError("image_size " + std::to_string(p.s) + " exceeds the supported 32768");
+  if (p.na * p.nd > (int64_t(1) << 31)) throw ValidationError("n_angles * det_count exceeds 2^31 rays");
+
+  const int64_t s = p.s, na = p.na, nd = p.nd;
+  const bool fan = g.kind == RK_FANBEAM;
+
+  // angle_trig (projector.cpp:89-93)
+  std::vector<double2> trig(static_cast<size_t>(na));
+  for (int64_t a = 0; a < na; ++a) trig[size_t(a)] = make_double2(std::cos(p.angles[size_t(a)]), std::sin(p.angles[size_t(a)]));
+
+  // ----- forward ray table: forward_parallel_t / forward_fanbeam_t ray setup
+  std::vector<float4> rg(static_cast<size_t>(na * nd));
+  std::vector<float2> rl(static_cast<size_t>(na * nd));
+  const double inf = std::numeric_limits<double>::infinity();
+  int64_t total = 0;
+  for (int64_t a = 0; a < na; ++a) {
+    double c = trig[size_t(a)].x, sn = trig[size_t(a)].y;
+    double sx = g.source_distance * sn;  // projector.cpp:123-124
+    double sy = -g.source_distance * c;
+    for (int64_t k = 0; k < nd; ++k) {
+      double u = (double(k) - 0.5 * double(nd) + 0.5) * g.det_spacing;
+      RaySetup r;
+      if (!fan) {
+        // projector.cpp:107-109: origin u*(c, s), direction (-s, c), t unbounded
+        r = setup_ray(s, u * c, u * sn, -sn, c, -inf, inf, g.step);
+      } else {
+        // projector.cpp:128-135: source -> detector cell, t in [0, len]
+        double px = u * c - g.det_distance * sn;
+        double py = u * sn + g.det_distance * c;
+        double dx = px - sx, dy = py - sy;
+        double len = std::sqrt(dx * dx + dy * dy);
+        r = setup_ray(s, sx, sy, dx / len, dy / len, 0.0, len, g.step);
+      }
+      if (r.n > (int64_t(1) << 30)) throw ValidationError("projector step too small: ray sample count overflows");
+      rg[size_t(a * nd + k)] = r.geom;
+      rl[size_t(a * nd + k)] = r.len;
+      total += r.n;
+    }
+  }
+  p.forward_samples = total;
+
+  // ----- backprojection staging window: the widest detector footprint of a
+  // 32x32 pixel tile over all tiles and angles (+ one cell on each side for
+  // the second tap and rounding).  kf as in projector.cpp:153-154 / 186-188.
+  const double half = 0.5 * double(s);
+  const double off = 0.5 * double(nd) - 0.5;
+  const double span = g.source_distance + g.det_distance;
+  int64_t tiles = (s + kBpTile - 1) / kBpTile;
+  int64_t need = 0;
+  for (int64_t a = 0; a < na; ++a) {
+    double c = trig[size_t(a)].x, sn = trig[size_t(a)].y;
+    for (int64_t ty = 0; ty < tiles; ++ty) {
+      for (int64_t tx = 0; tx < tiles; ++tx) {
+        double x0 = double(tx * kBpTile) - half + 0.5, x1 = x0 + double(kBpTile - 1);
+        double y0 = half - double(ty * kBpTile) - 0.5, y1 = y0 - double(kBpTile - 1);
+        double lo = inf, hi = -inf;
+        for (double x : {x0, x1})
+          for (double y : {y0, y1}) {
+            double kf;
+            if (!fan) {
+              kf = (x * c + y * sn) / g.det_spacing + off;
+            } else {
+              double qx = x * c + y * sn, qy = -x * sn + y * c;
+              kf = (qx * span / (qy + g.source_distance)) / g.det_spacing + off;
+            }
+            lo = std::min(lo, kf);
+            hi = std::max(hi, kf);
+          }
+        int64_t w = int64_t(std::floor(hi)) - int64_t(std::floor(lo)) + 3;
+        need = std::max(need, w);
+      }
+      if (!fan) break;  // parallel: footprint width is translation invariant up to floor effects
+    }
+  }
+  if (!fan) need += 1;  // floor effects across tiles
+  need += 1;            // rounding margin
+  int64_t window = (need + 3) / 4 * 4;
+  if (window > 4096)
+    throw ValidationError("backprojection footprint of " + std::to_string(window) +
+                          " detector cells per 32x32 tile is too wide (source too close to the image)");
+  p.bp_window = int(window);
+  // angles per staging pass: keep the window slab near 32 KB
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(32, (32 * 1024) / (window * 16)));
+  p.bp_angle_chunk = int(chunk);
+
+  // ----- upload (device < 0: host-only plan, used for inspection on machines without a GPU)
+  if (p.device < 0) return;
+  RK_CUDA(cudaSetDevice(p.device));
+  p.ray_geom.reserve(rg.size() * sizeof(float4));
+  p.ray_len.reserve(rl.size() * sizeof(float2));
+  p.trig.reserve(trig.size() * sizeof(double2));
+  RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(p.ray_len.ptr, rl.data(), rl.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaEventCreateWithFlags(&p.scratch_free, cudaEventDisableTiming));
+}
+
+// ----------------------------------------------------------------- filter
+const char* filter_kind_name(int kind) {  // sino_filter.cpp:24-33
+  switch (kind) {
+    case RK_RAM_LAK: return "ram-lak";
+    case RK_SHEPP_LOGAN: return "shepp-logan";
+    case RK_COSINE: return "cosine";
+    case RK_HAMMING: return "hamming";
+    case RK_HANN: return "hann";
+  }
+  return "?";
+}
+
+int filter_kind_from_name(const std::string& name) {  // sino_filter.cpp:14-22
+  for (int k = RK_RAM_LAK; k <= RK_HANN; ++k)
+    if (name == filter_kind_name(k)) return k;
+  throw ValidationError("unknown filter '" + name + "' (expected ram-lak, shepp-logan, cosine, hamming, or hann)");
+}
+
+namespace {
+
+// sino_filter.cpp:43-60
+double window_gain(int kind, double nu) {
+  switch (kind) {
+    case RK_SHEPP_LOGAN: {
+      if (nu == 0.0) return 1.0;
+      double t = 0.5 * M_PI * nu;
+      return std::sin(t) / t;
+    }
+    case RK_COSINE: return std::cos(0.5 * M_PI * nu);
+    case RK_HAMMING: return 0.54 + 0.46 * std::cos(M_PI * nu);
+    case RK_HANN: return 0.5 + 0.5 * std::cos(M_PI * nu);
+    default: return 1.0;
+  }
+}
+
+// Real-input FFT in fp64 (the make_filter call of fft::rfft, sino_filter.cpp:81):
+// iterative radix-2 decimation in time, twiddles cos/sin((2 pi k)/n).  n is
+// always a power of two here (sino_filter.cpp:69).
+void rfft_pow2(const std::vector<double>& x, std::vector<std::complex<double>>& out) {
+  size_t n = x.size();
+  std::vector<std::complex<double>> a(n);
+  for (size_t i = 0; i < n; ++i) a[i] = {x[i], 0.0};
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    size_t h = len / 2, stride = n / len;
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < h; ++k) {
+        double ang = 2.0 * M_PI * double(k * stride) / double(n);
+        std::complex<double> w(std::cos(ang), -std::sin(ang));
+        std::complex<double> u = a[i + k];
+        std::complex<double> xv = a[i + k + h];
+        std::complex<double> v(xv.real() * w.real() - xv.imag() * w.imag(), xv.real() * w.imag() + xv.imag() * w.real());
+        a[i + k] = {u.real() + v.real(), u.imag() + v.imag()};
+        a[i + k + h] = {u.real() - v.real(), u.imag() - v.imag()};
+      }
+  }
+  out.assign(a.begin(), a.begin() + ptrdiff_t(n / 2 + 1));
+}
+
+}  // namespace
+
+// sino_filter.cpp:64-92
+void build_filter(Filter& f, int kind, int64_t det_count) {
+  if (kind < RK_RAM_LAK || kind > RK_HANN) throw ValidationError("unknown filter kind " + std::to_string(kind));
+  if (det_count < 2) throw ValidationError("det_count must be >= 2, got " + std::to_string(det_count));
+  int64_t n = 1;
+  while (n < 2 * det_count) n <<= 1;
+  n = std::max<int64_t>(n, 2);
+  if (n > 8192)
+    throw ValidationError("det_count " + std::to_string(det_count) + " pads to " + std::to_string(n) +
+                          " > 8192, beyond the shared-memory FFT of the filter kernel");
+  f.kind = kind;
+  f.det_count = det_count;
+  f.padded = n;
+  std::vector<double> kernel(size_t(n), 0.0);
+  kernel[0] = 0.25;
+  for (int64_t p = 1; p < n; ++p) {
+    int64_t m = std::min(p, n - p);
+    if (m % 2 == 1) kernel[size_t(p)] = -1.0 / (double(m) * double(m) * M_PI * M_PI);
+  }
+  std::vector<std::complex<double>> bins;
+  rfft_pow2(kernel, bins);
+  f.response.resize(size_t(n / 2 + 1));
+  f.response_f.resize(size_t(n / 2 + 1));
+  for (int64_t q = 0; q <= n / 2; ++q) {
+    double nu = double(q) / double(n / 2);
+    double v = 2.0 * bins[size_t(q)].real() * window_gain(kind, nu);
+    f.response[size_t(q)] = v;
+    f.response_f[size_t(q)] = float(v);
+  }
+  // forward twiddles exp(-2 pi i k / n), k < n/2, evaluated in fp64 and rounded
+  std::vector<float2> tw(static_cast<size_t>(std::max<int64_t>(n / 2, 1)));
+  for (int64_t k = 0; k < n / 2; ++k) {
+    double ang = 2.0 * M_PI * double(k) / double(n);
+    tw[size_t(k)] = make_float2(float(std::cos(ang)), float(-std::sin(ang)));
+  }
+  if (f.device < 0) return;  // host-only filter (response inspection without a GPU)
+  RK_CUDA(cudaSetDevice(f.device));
+  f.d_response.reserve(f.response_f.size() * sizeof(float));
+  f.d_twiddle.reserve(tw.size() * sizeof(float2));
+  RK_CUDA(cudaMemcpy(f.d_response.ptr, f.response_f.data(), f.response_f.size() * sizeof(float),
+                     cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(f.d_twiddle.ptr, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+}
+
+}  // namespace rk

@@ -1,0 +1,157 @@
+// Internal declarations shared by the host plan code, the C ABI and the
+// CUDA kernels of the B200 Radon projector.  Not part of the public ABI
+// (include/radon_b200.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "radon_b200.h"
+
+namespace rk {
+
+// ----------------------------------------------------------------- errors
+// Mirrors the reference's exception taxonomy (errors.hpp:9-40); the C ABI
+// maps them onto rk_status codes.
+struct ValidationError : std::invalid_argument {
+  explicit ValidationError(const std::string& w) : std::invalid_argument(w) {}
+};
+struct NumericalError : std::runtime_error {
+  explicit NumericalError(const std::string& w, long it = -1) : std::runtime_error(w), iteration(it) {}
+  long iteration;
+};
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define RK_CUDA(call) ::rk::cuda_check((call), #call)
+
+// ----------------------------------------------------------------- device buffers
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() { release(); }
+  void release();
+  // grows (never shrinks); contents are not preserved
+  void reserve(size_t n);
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+// ----------------------------------------------------------------- layouts
+// Packed ("image-interleaved") layouts used inside the library.  Four batch
+// elements share one 16-byte texel so that one 128-bit shared-memory load
+// delivers a tap for four images: the index/weight arithmetic of a ray
+// sample or pixel/angle pair is paid once per four images.
+//   image : [G][s+2][s+2] float4, one zero texel of border on every side
+//           (the reference's zero padding, projector.cpp:57-60)
+//   sino  : [G][n_angles][det_count] float4
+// with G = ceil(batch / 4); missing images of the last group are zero.
+constexpr int kPack = 4;
+
+inline int64_t groups_of(int64_t batch) { return (batch + kPack - 1) / kPack; }
+
+// ----------------------------------------------------------------- plan
+struct Plan {
+  int device = 0;
+  rk_geometry g{};              // resolved; g.angles -> angles.data()
+  std::vector<double> angles;
+  int64_t s = 0, na = 0, nd = 0;
+  int64_t forward_samples = 0;  // exact algorithmic work per image
+
+  // forward: one record per ray (a * nd + k), built in fp64 on the host
+  DeviceBuffer ray_geom;   // float4 {px0, py0, hx, hy} in padded pixel coordinates
+  DeviceBuffer ray_len;    // float2 {h, n (int bits)}
+  // backprojection: per-angle trig in fp64
+  DeviceBuffer trig;       // double2 {cos, sin}
+  int bp_window = 0;       // staged detector cells per (tile, angle)
+  int bp_angle_chunk = 0;  // angles staged per pass
+
+  // scratch (serialised by `mu`; `scratch_free` orders reuse across streams)
+  std::mutex mu;
+  DeviceBuffer packed_image, packed_sino;
+  cudaEvent_t scratch_free = nullptr;
+  // host-buffer (*_host) pipelines: two streams, each with its own buffers
+  cudaStream_t copy_streams[2] = {nullptr, nullptr};
+  DeviceBuffer pipe_in[2], pipe_out[2], pipe_pk[2];
+  // solver scratch
+  DeviceBuffer solver_a, solver_b, solver_c, solver_d, solver_scalars;
+
+  ~Plan();
+};
+
+struct Filter {
+  int device = 0;
+  int kind = 0;
+  int64_t det_count = 0;
+  int64_t padded = 0;
+  std::vector<double> response;   // padded/2+1 bins (double)
+  std::vector<float> response_f;  // same, float (sino_filter.cpp:89)
+  DeviceBuffer d_response;        // float, padded/2+1
+  DeviceBuffer d_twiddle;         // float2, padded/2 (forward twiddles)
+  std::mutex mu;
+};
+
+// ----------------------------------------------------------------- host helpers (plan.cpp)
+rk_geometry resolve_geometry(const rk_geometry& in);
+void build_plan(Plan& p);
+void build_filter(Filter& f, int kind, int64_t det_count);
+const char* filter_kind_name(int kind);
+int filter_kind_from_name(const std::string& name);
+
+// ----------------------------------------------------------------- launchers (kernels.cu / filter.cu)
+// All launchers enqueue on `stream` and never synchronise.
+void launch_pack_images(int dtype, const void* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
+void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int64_t nd, float4* dst,
+                      cudaStream_t st);
+void launch_forward(const Plan& p, const float4* packed_image, int64_t batch, int dtype, void* sino,
+                    cudaStream_t st);
+void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch, int dtype, void* image,
+                        cudaStream_t st);
+// filter: rows of det_count in `dtype`; writes either the user layout
+// (`out`, dtype) or, when `packed_out` is set, the packed sino layout.
+void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, int64_t n_angles, void* out,
+                   float4* packed_out, cudaStream_t st);
+
+size_t dtype_size(int dtype);
+
+// ----------------------------------------------------------------- instrumentation (profiling.cu)
+constexpr int kKernelKinds = RK_KERNEL_KINDS;
+// Counts the launch; when profiling is enabled also records start/stop events
+// on `st` around the scope (construct right before the <<<>>> launch).
+class KernelTimer {
+ public:
+  KernelTimer(int kind, cudaStream_t st);
+  ~KernelTimer();
+  KernelTimer(const KernelTimer&) = delete;
+  KernelTimer& operator=(const KernelTimer&) = delete;
+
+ private:
+  int kind_;
+  cudaStream_t st_;
+  cudaEvent_t start_ = nullptr, stop_ = nullptr;
+  bool active_ = false;
+};
+void profiling_enable(bool on);
+void profiling_read(rk_kernel_stats* out, bool reset);
+double probe_smem_bandwidth(int device);
+
+}  // namespace rk
+
+struct rk_plan {
+  rk::Plan p;
+};
+struct rk_filter {
+  rk::Filter f;
+};

@@ -1,0 +1,209 @@
+"""GPU parity of forward / backprojection against the reference oracle.
+
+Restates the projector assertions of proj/tests/test_projector.cpp and
+acceptance.cpp (criteria 4, 9) on the B200 kernels, plus oracle parity at
+rel-L2 <= 1e-5 (fp32) / 1e-3 (fp16) as the north star requires.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import Geom, batched_phantom, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 1e-5  # north star: fp32 storage vs the CPU reference
+TOL16 = 1e-3  # north star: fp16 storage
+
+
+def par(rk, s, na, det=None, spacing=None):
+    return rk.make_parallel(s, rk.angles_linspace(0.0, np.pi, na), det, spacing)
+
+
+def fan(rk, s, na, src, **kw):
+    return rk.make_fanbeam(s, rk.angles_linspace(0.0, 2 * np.pi, na), src, **kw)
+
+
+def ogeom(g, step=1.0):
+    if hasattr(g, "source_distance"):
+        return Geom("fanbeam", g.image_size, np.asarray(g.angles), g.det_count, g.det_spacing, g.source_distance,
+                    g.det_distance, step)
+    return Geom("parallel", g.image_size, np.asarray(g.angles), g.det_count, g.det_spacing, step=step)
+
+
+def dev(a, cuda):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+CASES = [
+    ("par-32-45", lambda rk: par(rk, 32, 45)),
+    ("par-64-90-det96", lambda rk: par(rk, 64, 90, 96)),
+    ("par-100-33-det77-sp1.3", lambda rk: par(rk, 100, 33, 77, 1.3)),
+    ("fan-32-24-D64", lambda rk: fan(rk, 32, 24, 64.0)),
+    ("fan-64-90-D128", lambda rk: fan(rk, 64, 90, 128.0)),
+    ("fan-80-40-D60-dd150-det101", lambda rk: fan(rk, 80, 40, 60.0, det_distance=150.0, det_count=101)),
+]
+
+
+@pytest.mark.parametrize("name,mk", CASES, ids=[c[0] for c in CASES])
+def test_parity_fp32(rk, oracle, cuda, name, mk):
+    g = mk(rk)
+    B = 5
+    img = batched_phantom(oracle, g.image_size, B)
+    img[2] = oracle.rng_uniform(2024, g.image_size ** 2).reshape(g.image_size, g.image_size)
+    sino = rk.forward(g, dev(img, cuda))
+    ref_sino = oracle.forward(ogeom(g), img)
+    assert sino.dtype == torch.float32 and tuple(sino.shape) == ref_sino.shape
+    assert rel_l2(host(sino), ref_sino) <= TOL32
+    bp = rk.backprojection(g, dev(ref_sino, cuda))
+    ref_bp = oracle.backprojection(ogeom(g), ref_sino)
+    assert rel_l2(host(bp), ref_bp) <= TOL32
+
+
+@pytest.mark.parametrize("name,mk", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_parity_fp16_and_fp64_storage(rk, oracle, cuda, name, mk):
+    g = mk(rk)
+    img = batched_phantom(oracle, g.image_size, 3)
+    for dt, tol in ((np.float16, TOL16), (np.float64, TOL32)):
+        x = img.astype(dt)
+        sino = rk.forward(g, dev(x, cuda))
+        assert host(sino).dtype == dt  # output keeps the input precision (test_projector.cpp:206-214)
+        ref_sino = oracle.forward(ogeom(g), x)
+        assert rel_l2(host(sino), ref_sino) <= tol
+        bp = rk.backprojection(g, dev(ref_sino, cuda))
+        assert rel_l2(host(bp), oracle.backprojection(ogeom(g), ref_sino)) <= tol
+
+
+def test_config1_parity(rk, oracle, cuda):
+    """parallel 256/256/256, batch 8, fp32; phantom batch and Rng(2024) uniform."""
+    g = par(rk, 256, 256)
+    for img in (batched_phantom(oracle, 256, 8),
+                oracle.rng_uniform(2024, 8 * 256 * 256).reshape(8, 256, 256)):
+        sino = rk.forward(g, dev(img, cuda))
+        ref_sino = oracle.forward(ogeom(g), img)
+        assert rel_l2(host(sino), ref_sino) <= TOL32
+        bp = rk.backprojection(g, sino)
+        ref_bp = oracle.backprojection(ogeom(g), ref_sino)
+        assert rel_l2(host(bp), ref_bp) <= TOL32
+
+
+def test_zero_maps_to_zero(rk, cuda):
+    """test_projector.cpp:44-55."""
+    for s in (8, 32):
+        for g in (par(rk, s, 10), fan(rk, s, 10, 2.0 * s)):
+            zi = torch.zeros(1, s, s, device=cuda)
+            zs = torch.zeros(1, 10, s, device=cuda)
+            assert float(rk.forward(g, zi).abs().sum()) == 0.0
+            assert float(rk.backprojection(g, zs).abs().sum()) == 0.0
+
+
+def test_axis_aligned_closed_forms(rk, oracle, cuda):
+    """test_projector.cpp:135-164."""
+    s = 16
+    img = oracle.shepp_logan(s, np.float64)
+    g = rk.make_parallel(s, [0.0])
+    f = host(rk.forward(g, dev(img, cuda)))[0, 0]
+    np.testing.assert_allclose(f, img[0].sum(axis=0), rtol=1e-6, atol=1e-6)
+    delta = np.zeros((1, 1, s))
+    delta[0, 0, 5] = 1.0
+    bp = host(rk.backprojection(g, dev(delta, cuda)))[0]
+    assert np.all(bp[:, 5] == 1.0) and np.all(np.delete(bp, 5, axis=1) == 0.0)
+    gw = par(rk, 32, 90, 48)
+    bp = host(rk.backprojection(gw, torch.ones(1, 90, 48, device=cuda)))
+    np.testing.assert_allclose(bp, 90.0, rtol=1e-6)
+
+
+def test_opposite_angles_reverse_detector(rk, oracle, cuda):
+    """test_projector.cpp:166-181."""
+    s, na, det = 64, 12, 80
+    both = rk.angles_linspace(0.0, np.pi, na)
+    both = both + [a + np.pi for a in both]
+    g = rk.make_parallel(s, both, det)
+    f = host(rk.forward(g, dev(oracle.shepp_logan(s), cuda)))[0]
+    assert rel_l2(f[na:, ::-1], f[:na]) < 1e-5
+
+
+def test_linearity(rk, oracle, cuda):
+    """test_projector.cpp:183-194 at fp32 roundoff."""
+    g = par(rk, 32, 20)
+    a = oracle.rng_uniform(3, 32 * 32, True).reshape(1, 32, 32).astype(np.float64)
+    b = oracle.rng_uniform(4, 32 * 32, True).reshape(1, 32, 32).astype(np.float64)
+    lhs = host(rk.forward(g, dev(2.0 * a - 0.5 * b, cuda)))
+    rhs = 2.0 * host(rk.forward(g, dev(a, cuda))) - 0.5 * host(rk.forward(g, dev(b, cuda)))
+    assert rel_l2(lhs, rhs) < 1e-5
+
+
+def test_fan_far_source_approaches_parallel(rk, oracle, cuda):
+    """test_projector.cpp:196-204."""
+    img = dev(oracle.shepp_logan(64), cuda)
+    ang = rk.angles_linspace(0.0, np.pi, 48)
+    fp = host(rk.forward(rk.make_parallel(64, ang), img))
+    ff = host(rk.forward(rk.make_fanbeam(64, ang, 1e6), img))
+    assert rel_l2(ff, fp) < 1e-3
+
+
+def test_batched_equals_per_element_bitwise(rk, oracle, cuda):
+    """test_projector.cpp:234-250 / acceptance.cpp:340-389 (C9)."""
+    s, B = 32, 7
+    imgs = dev(batched_phantom(oracle, s, B), cuda)
+    for g in (par(rk, s, 24), fan(rk, s, 24, 64.0)):
+        fb = rk.forward(g, imgs)
+        bb = rk.backprojection(g, fb)
+        for e in range(B):
+            fe = rk.forward(g, imgs[e:e + 1])
+            assert torch.equal(fb[e:e + 1], fe)
+            assert torch.equal(bb[e:e + 1], rk.backprojection(g, fe))
+
+
+def test_quadrature_step(rk, oracle, cuda):
+    """test_projector.cpp:268-279 + oracle parity at step 0.5."""
+    img = oracle.shepp_logan(32, np.float64)
+    g = par(rk, 32, 16)
+    f1 = host(rk.forward(g, dev(img, cuda)))
+    fh = host(rk.forward(g, dev(img, cuda), rk.ProjectorOptions(0.5)))
+    rel = rel_l2(fh, f1)
+    assert 0.0 < rel < 0.05
+    assert rel_l2(fh, oracle.forward(ogeom(g, 0.5), img)) <= TOL32
+    with pytest.raises(rk.ValidationError):
+        rk.forward(g, dev(img, cuda), rk.ProjectorOptions(0.0))
+    with pytest.raises(rk.ValidationError):
+        rk.forward(g, dev(img, cuda), rk.ProjectorOptions(-1.0))
+
+
+def test_shape_validation(rk, cuda):
+    """test_projector.cpp:281-288."""
+    g = par(rk, 32, 10)
+    for bad in ((1, 16, 16), (32, 32)):
+        with pytest.raises(rk.ValidationError):
+            rk.forward(g, torch.zeros(*bad, device=cuda))
+    for bad in ((1, 10, 16), (1, 5, 32), (10, 32)):
+        with pytest.raises(rk.ValidationError):
+            rk.backprojection(g, torch.zeros(*bad, device=cuda))
+
+
+def test_host_path_matches_device_path(rk, oracle, cuda):
+    """*_host entry points (reference-shaped host buffers, pipelined copies) == device entry points."""
+    g = par(rk, 64, 40)
+    img = batched_phantom(oracle, 64, 13)
+    sd = host(rk.forward(g, dev(img, cuda)))
+    sh = rk.forward(g, img)  # numpy in -> numpy out through rk_forward_host
+    assert isinstance(sh, np.ndarray) and np.array_equal(sd, sh)
+    pinned = torch.from_numpy(sh).pin_memory()
+    bh = rk.backprojection(g, pinned)
+    assert torch.equal(bh, rk.backprojection(g, dev(sh, cuda)).cpu())
+
+
+def test_half_accuracy_vs_single(rk, oracle, cuda):
+    """acceptance.cpp:212-235 (C4) / test_projector.cpp:226-231: fp16 storage within 5e-4 of fp32."""
+    g = par(rk, 256, 256)
+    p = oracle.shepp_logan(256)
+    fs = host(rk.forward(g, dev(p, cuda)))
+    fh = host(rk.forward(g, dev(p.astype(np.float16), cuda)))
+    assert rel_l2(fh, fs) <= 5e-4
+    bs = host(rk.backprojection(g, dev(fs, cuda)))
+    bh = host(rk.backprojection(g, dev(fs.astype(np.float16), cuda)))
+    assert rel_l2(bh, bs) < 1e-3
