@@ -71,10 +71,14 @@ void check_device_filter(const rk_filter* f) {
 
 // Device-pointer bodies, reused by the host-buffer pipelines with their own scratch.
 void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
-                  cudaStream_t st) {
+                  rk::DeviceBuffer& pkt, cudaStream_t st) {
   pk.reserve(packed_image_bytes(p, batch));
   rk::launch_pack_images(dtype, d_image, batch, p.s, pk.as<float4>(), st);
-  rk::launch_forward(p, pk.as<float4>(), batch, dtype, d_sino, st);
+  if (p.fwd.any_transposed) {
+    pkt.reserve(packed_image_bytes(p, batch));
+    rk::launch_transpose_images(pk.as<float4>(), batch, p.s, pkt.as<float4>(), st);
+  }
+  rk::launch_forward(p, pk.as<float4>(), pkt.as<float4>(), batch, dtype, d_sino, st);
 }
 
 void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
@@ -134,7 +138,7 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
     const char* src = static_cast<const char*>(h_in) + size_t(b0) * in_item;
     char* dst = static_cast<char*>(h_out) + size_t(b0) * out_item;
     RK_CUDA(cudaMemcpyAsync(p.pipe_in[slot].ptr, src, size_t(nb) * in_item, cudaMemcpyHostToDevice, st));
-    body(p.pipe_in[slot].ptr, nb, p.pipe_out[slot].ptr, p.pipe_pk[slot], st);
+    body(p.pipe_in[slot].ptr, nb, p.pipe_out[slot].ptr, slot, st);
     RK_CUDA(cudaMemcpyAsync(dst, p.pipe_out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
     if (!pinned_in || !pinned_out) RK_CUDA(cudaStreamSynchronize(st));
   }
@@ -218,7 +222,7 @@ int rk_forward(rk_plan* plan, int dtype, const void* d_image, int64_t batch, voi
     require(d_image != nullptr && d_sino != nullptr, "image / sinogram pointer is null");
     rk::Plan& p = plan->p;
     ScratchLease lease(p, as_stream(stream));
-    forward_into(p, dtype, d_image, batch, d_sino, p.packed_image, as_stream(stream));
+    forward_into(p, dtype, d_image, batch, d_sino, p.packed_image, p.packed_image_t, as_stream(stream));
   });
 }
 
@@ -321,8 +325,8 @@ int rk_forward_host(rk_plan* plan, int dtype, const void* h_image, int64_t batch
     rk::Plan& p = plan->p;
     const size_t es = rk::dtype_size(dtype);
     run_host_pipeline(p, batch, size_t(p.s * p.s) * es, size_t(p.na * p.nd) * es, h_image, h_sino,
-                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
-                        forward_into(p, dtype, din, nb, dout, pk, st);
+                      [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
+                        forward_into(p, dtype, din, nb, dout, p.pipe_pk[slot], p.pipe_pkt[slot], st);
                       });
   });
 }
@@ -336,8 +340,8 @@ int rk_backproject_host(rk_plan* plan, int dtype, const void* h_sino, int64_t ba
     rk::Plan& p = plan->p;
     const size_t es = rk::dtype_size(dtype);
     run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
-                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
-                        backproject_into(p, dtype, din, nb, dout, pk, st);
+                      [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
+                        backproject_into(p, dtype, din, nb, dout, p.pipe_pk[slot], st);
                       });
   });
 }
@@ -374,8 +378,8 @@ int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino,
                                              " does not match filter " + std::to_string(filter->f.det_count));
     const size_t es = rk::dtype_size(dtype);
     run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
-                      [&](const void* din, int64_t nb, void* dout, rk::DeviceBuffer& pk, cudaStream_t st) {
-                        fbp_into(p, filter->f, dtype, din, nb, dout, pk, st);
+                      [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
+                        fbp_into(p, filter->f, dtype, din, nb, dout, p.pipe_pk[slot], st);
                       });
   });
 }

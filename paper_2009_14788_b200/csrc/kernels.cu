@@ -8,6 +8,8 @@
 // equal per-element results bit for bit (acceptance.cpp:340-389).
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "rk_internal.hpp"
 
 namespace rk {
@@ -84,49 +86,132 @@ __global__ void pack_sino_kernel(const T* __restrict__ src, int64_t batch, int64
 }
 
 // ------------------------------------------------------------------ forward
-// One thread per (ray, image group): ray march with software bilinear
-// interpolation (projector.cpp:47-83).  The clipped entry point, step and
-// sample count come from the fp64 ray table; sample m sits at
-// (px0, py0) + (m + 0.5) * (hx, hy) in padded pixel coordinates, exactly
-// the reference's t_m = t0 + (m + 0.5) h.  Taps of four images are read as
-// one float4 each; the 4-tap weights are shared by the four images.
-template <class TOut>
-__global__ void __launch_bounds__(256) forward_kernel(const float4* __restrict__ img, int s,
-                                                      const float4* __restrict__ ray_geom,
-                                                      const float2* __restrict__ ray_len, int64_t n_rays,
-                                                      int64_t batch, TOut* __restrict__ sino) {
-  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n_rays) return;
-  const int P = s + 2;
-  const int64_t g = blockIdx.y;
-  const float4* im = img + g * int64_t(P) * P;
-  const float4 R = __ldg(ray_geom + r);
-  const float2 L = __ldg(ray_len + r);
-  const int n = __float_as_int(L.y);
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  for (int m = 0; m < n; ++m) {
-    const float t = float(m) + 0.5f;
-    const float px = fmaf(t, R.z, R.x);
-    const float py = fmaf(t, R.w, R.y);
-    const float fj = floorf(px), fi = floorf(py);
-    const float fx = px - fj, fy = py - fi;
-    const int j0 = min(max(int(fj), 0), P - 2);
-    const int i0 = min(max(int(fi), 0), P - 2);
-    const float4* p = im + i0 * P + j0;
-    const float4 v00 = __ldg(p), v01 = __ldg(p + 1), v10 = __ldg(p + P), v11 = __ldg(p + P + 1);
-    const float gx = 1.f - fx, gy = 1.f - fy;
-    const float w00 = gx * gy, w01 = fx * gy, w10 = gx * fy, w11 = fx * fy;
-    a0 = fmaf(w00, v00.x, fmaf(w01, v01.x, fmaf(w10, v10.x, fmaf(w11, v11.x, a0))));
-    a1 = fmaf(w00, v00.y, fmaf(w01, v01.y, fmaf(w10, v10.y, fmaf(w11, v11.y, a1))));
-    a2 = fmaf(w00, v00.z, fmaf(w01, v01.z, fmaf(w10, v10.z, fmaf(w11, v11.z, a2))));
-    a3 = fmaf(w00, v00.w, fmaf(w01, v01.w, fmaf(w10, v10.w, fmaf(w11, v11.w, a3))));
+// packed image -> transposed packed image, 32x32-texel tiles through shared
+// memory (coalesced both ways).
+__global__ void transpose_images_kernel(const float4* __restrict__ src, int P, float4* __restrict__ dst) {
+  __shared__ float4 tile[32][33];
+  const int64_t plane = int64_t(P) * P;
+  const float4* s = src + blockIdx.z * plane;
+  float4* d = dst + blockIdx.z * plane;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, j = bx + threadIdx.x;
+    if (i < P && j < P) tile[r][threadIdx.x] = s[int64_t(i) * P + j];
   }
-  const float h = L.x;
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + r, j = by + threadIdx.x;  // dst row = src column
+    if (i < P && j < P) d[int64_t(i) * P + j] = tile[threadIdx.x][r];
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (lanes)
+
+// Ray-driven forward projection (projector.cpp:66-139), one CTA per block of
+// 8 angles x 32 detector cells and per packed group of four images.  All rays
+// of the CTA march together chunk by chunk along t; before each chunk the
+// box of padded-image texels its samples can touch (fwd_plan.cpp) is copied
+// to shared memory with cp.async, then each lane runs its own samples of the
+// chunk: sample m at (px0, py0) + (m + 0.5) (hx, hy) — the reference's
+// t_m = t0 + (m + 0.5) h — bilinear taps as four 128-bit shared loads (one
+// tap of four images each), weights shared by the four images.  Samples are
+// visited in ascending m, so each output is a fixed-order fp32 sum.
+// Chunk membership: m < ceil((T_{c+1} - t0) / h - 0.5), evaluated in fp32;
+// the boxes carry one unit of slack in t, so rounding never leaves a sample
+// outside its box.  CTAs whose lanes spread mostly along image columns read
+// the transposed packed image with x and y swapped (bilinear is symmetric).
+template <class TOut>
+__global__ void __launch_bounds__(kFwdThreads, 2) forward_kernel(
+    const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
+    const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int2* __restrict__ cta_cfg, int na,
+    int nd, int chunks, float tbase, float tlen, int ctas_k, int64_t batch, TOut* __restrict__ sino,
+    FwdEpilogue epi) {
+  extern __shared__ float4 box_s[];
+  const int cta = blockIdx.x;
+  const int ga = cta / ctas_k, gk = cta - ga * ctas_k;
+  const int64_t g = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = ga * (kFwdThreads / 32) + warp, k = gk * 32 + lane;
+  const bool valid = a < na && k < nd;
+  const int64_t r = int64_t(a) * nd + k;
+  const int2 cfg = cta_cfg[cta];
+  const int pitch = cfg.x;
+  const bool tr = cfg.y != 0;
+  float4 G = make_float4(0.f, 0.f, 0.f, 0.f), X = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    G = __ldg(ray_geom + r);
+    X = __ldg(ray_aux + r);
+  }
+  const float px0 = tr ? G.y : G.x, py0 = tr ? G.x : G.y;
+  const float hx = tr ? G.w : G.z, hy = tr ? G.z : G.w;
+  const int n = __float_as_int(X.y);
+  const float t0 = X.z, inv_h = X.w;
+  const int P = s + 2;
+  const float4* src = (tr ? img_t : img) + g * int64_t(P) * P;
+  const int4* bxs = boxes + int64_t(cta) * chunks;
+
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int m = 0;
+  for (int c = 0; c < chunks; ++c) {
+    const int4 bx = __ldg(bxs + c);  // CTA-uniform
+    if (bx.z == 0) continue;
+    int m_end = n;
+    if (c + 1 < chunks) {
+      const float tn = fmaf(float(c + 1), tlen, tbase);
+      m_end = min(max(int(ceilf(fmaf(tn - t0, inv_h, -0.5f))), 0), n);
+    }
+    __syncthreads();  // previous chunk's samples are done with the box
+    for (int rr = warp; rr < bx.z; rr += kFwdThreads / 32) {
+      const float4* srow = src + int64_t(bx.x + rr) * P + bx.y;
+      float4* drow = box_s + rr * pitch;
+      for (int cc = lane; cc < bx.w; cc += 32) cp_async16(drow + cc, srow + cc);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const float ox = float(bx.y), oy = float(bx.x);
+    const int jmax = bx.w - 2, imax = bx.z - 2;
+    for (; m < m_end; ++m) {
+      const float t = float(m) + 0.5f;
+      const float px = fmaf(t, hx, px0) - ox;  // exact shift: the box origin is an integer
+      const float py = fmaf(t, hy, py0) - oy;
+      const float fj = floorf(px), fi = floorf(py);
+      const float fx = px - fj, fy = py - fi;
+      const int j = min(max(int(fj), 0), jmax);
+      const int i = min(max(int(fi), 0), imax);
+      const float4* q = box_s + i * pitch + j;
+      const float4 v00 = q[0], v01 = q[1], v10 = q[pitch], v11 = q[pitch + 1];
+      const float gx = 1.f - fx, gy = 1.f - fy;
+      const float w00 = gx * gy, w01 = fx * gy, w10 = gx * fy, w11 = fx * fy;
+      a0 = fmaf(w00, v00.x, fmaf(w01, v01.x, fmaf(w10, v10.x, fmaf(w11, v11.x, a0))));
+      a1 = fmaf(w00, v00.y, fmaf(w01, v01.y, fmaf(w10, v10.y, fmaf(w11, v11.y, a1))));
+      a2 = fmaf(w00, v00.z, fmaf(w01, v01.z, fmaf(w10, v10.z, fmaf(w11, v11.z, a2))));
+      a3 = fmaf(w00, v00.w, fmaf(w01, v01.w, fmaf(w10, v10.w, fmaf(w11, v11.w, a3))));
+    }
+  }
+  if (!valid) return;
+  const float h = X.x;
   const float acc[kPack] = {a0 * h, a1 * h, a2 * h, a3 * h};
+  const int64_t n_rays = int64_t(na) * nd;
+  if (epi.mode == kOutUser) {
 #pragma unroll
-  for (int q = 0; q < kPack; ++q) {
-    const int64_t b = g * kPack + q;
-    if (b < batch) sino[b * n_rays + r] = from_f32<TOut>(acc[q]);
+    for (int q = 0; q < kPack; ++q) {
+      const int64_t b = g * kPack + q;
+      if (b < batch) sino[b * n_rays + r] = from_f32<TOut>(acc[q]);
+    }
+  } else {
+    // packed sinogram for the solvers; kOutResidual subtracts y (solvers.cpp:136: A x - y)
+    float4 v = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    if (epi.mode == kOutResidual) {
+      const float4 y = __ldg(epi.resid + g * n_rays + r);
+      v = make_float4(v.x - y.x, v.y - y.y, v.z - y.z, v.w - y.w);
+    }
+    epi.packed[g * n_rays + r] = v;
   }
 }
 
@@ -138,10 +223,23 @@ __global__ void __launch_bounds__(256) forward_kernel(const float4* __restrict__
 // memory (zero outside [0, det_count), which is the reference's skipped-tap
 // rule, projector.cpp:159-162), then every pixel accumulates its two-tap
 // lerp for each angle in ascending angle order (projector.cpp:152-163).
-struct AngleConst {
-  float a, b, c, d;  // parallel: base, cx, cy, -; fan: qx00, den00, offw, -
-  float e, f, g, h;  // fan: cos, sin, -, -
+// Per-angle constants of one tile.  Parallel beam: kf - ws is affine in the
+// pixel offsets, fp32 suffices (no magnification).  Fan beam: the pixel ->
+// detector map u = qx * span / (qy + D_so) magnifies position errors by
+// span / (qy + D_so) (large near the source), so the per-pixel geometry runs
+// in fp64 (B200's fp64 rate keeps it off the critical path).
+struct ParConst {
+  float base, cx, cy, pad;
 };
+struct FanConst {
+  double qx00, den00, c, s, offw, pad;
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 constexpr int kTile = 32;
 constexpr int kRowsPerThread = 4;
@@ -151,11 +249,12 @@ template <bool FAN, class TOut>
 __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, int window, int chunk, int64_t batch,
-    TOut* __restrict__ out) {
+    TOut* __restrict__ out, BpEpilogue epi) {
+  using Const = typename std::conditional<FAN, FanConst, ParConst>::type;
   extern __shared__ float4 smem[];
-  float4* win = smem;                                                      // chunk * window cells
-  AngleConst* cst = reinterpret_cast<AngleConst*>(smem + size_t(chunk) * window);  // chunk records
-  int* ws_s = reinterpret_cast<int*>(cst + chunk);                          // chunk window starts
+  float4* win = smem;                                                    // chunk * window cells
+  Const* cst = reinterpret_cast<Const*>(smem + size_t(chunk) * window);  // chunk records
+  int* ws_s = reinterpret_cast<int*>(cst + chunk);                        // chunk window starts
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kTile + tx;
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile;
@@ -178,21 +277,22 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
     if (tid < nac) {
       const double2 cs = trig[a0 + tid];
       const double c = cs.x, sn = cs.y;
-      const double x1 = x0 + double(kTile - 1), y1 = y0 - double(kTile - 1);
+      // last in-image pixel of the tile: the footprint extremes sit at the
+      // corners only where qy + D_so keeps its sign, i.e. inside the image
+      const double x1 = x0 + double(min(kTile, s - j0) - 1), y1 = y0 - double(min(kTile, s - i0) - 1);
       double lo;
-      AngleConst k;
-      if (!FAN) {
+      Const k;
+      if constexpr (!FAN) {
         const double k00 = (x0 * c + y0 * sn) / spacing + off;
         const double k10 = (x1 * c + y0 * sn) / spacing + off;
         const double k01 = (x0 * c + y1 * sn) / spacing + off;
         const double k11 = (x1 * c + y1 * sn) / spacing + off;
         lo = fmin(fmin(k00, k10), fmin(k01, k11));
-        const int ws = int(floor(lo)) - 1;
-        k.a = float(k00 - double(ws));
-        k.b = float(c / spacing);
-        k.c = float(-sn / spacing);
-        k.d = 0.f;
-        k.e = k.f = k.g = k.h = 0.f;
+        const int ws = max(int(floor(lo)) - 1, -2);  // clipped like the host window (plan.cpp)
+        k.base = float(k00 - double(ws));
+        k.cx = float(c / spacing);
+        k.cy = float(-sn / spacing);
+        k.pad = 0.f;
         ws_s[tid] = ws;
       } else {
         auto kfan = [&](double x, double y) {
@@ -200,16 +300,13 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
           return (qx * span / (qy + source_distance)) / spacing + off;
         };
         lo = fmin(fmin(kfan(x0, y0), kfan(x1, y0)), fmin(kfan(x0, y1), kfan(x1, y1)));
-        const int ws = int(floor(lo)) - 1;
-        const double qx00 = x0 * c + y0 * sn;
-        const double den00 = -x0 * sn + y0 * c + source_distance;
-        k.a = float(qx00);
-        k.b = float(den00);
-        k.c = float(off - double(ws));
-        k.d = 0.f;
-        k.e = float(c);
-        k.f = float(sn);
-        k.g = k.h = 0.f;
+        const int ws = max(int(floor(lo)) - 1, -2);  // clipped like the host window (plan.cpp)
+        k.qx00 = x0 * c + y0 * sn;
+        k.den00 = -x0 * sn + y0 * c + source_distance;
+        k.c = c;
+        k.s = sn;
+        k.offw = off - double(ws);
+        k.pad = 0.0;
         ws_s[tid] = ws;
       }
       cst[tid] = k;
@@ -225,20 +322,23 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
     }
     __syncthreads();
     // ---- accumulate
-    const float fspan = float(span / spacing);
+    const double kmag = span / spacing;
     for (int q = 0; q < nac; ++q) {
-      const AngleConst k = cst[q];
+      const Const k = cst[q];
       const float4* w = win + q * window;
 #pragma unroll
       for (int r = 0; r < kRowsPerThread; ++r) {
         const float lx = float(tx), ly = float(ty + r * (kTile / kRowsPerThread));
         float kf;
-        if (!FAN) {
-          kf = fmaf(lx, k.b, fmaf(ly, k.c, k.a));
+        if constexpr (!FAN) {
+          kf = fmaf(lx, k.cx, fmaf(ly, k.cy, k.base));
         } else {
-          const float qx = fmaf(lx, k.e, fmaf(-ly, k.f, k.a));
-          const float den = fmaf(-lx, k.f, fmaf(-ly, k.e, k.b));
-          kf = fmaf(qx * fspan, __frcp_rn(den), k.c);
+          const double dlx = double(lx), dly = double(ly);
+          const double qx = fma(dlx, k.c, fma(-dly, k.s, k.qx00));
+          const double den = fma(-dlx, k.s, fma(-dly, k.c, k.den00));
+          double r = double(rcp_approx(float(den)));
+          r = fma(r, fma(-den, r, 1.0), r);  // one Newton step: ~1e-14 relative
+          kf = float(fma(qx * kmag, r, k.offw));
         }
         const float fk = floorf(kf);
         const float wt = kf - fk;
@@ -254,15 +354,36 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
     __syncthreads();
   }
   // ---- store
+  const int P = s + 2;
 #pragma unroll
   for (int r = 0; r < kRowsPerThread; ++r) {
     const int i = i0 + ty + r * (kTile / kRowsPerThread), j = j0 + tx;
     if (i >= s || j >= s) continue;
-    const float v[kPack] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
+    if (epi.mode == kOutUser) {
+      const float v[kPack] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
 #pragma unroll
-    for (int q = 0; q < kPack; ++q) {
-      const int64_t b = g * kPack + q;
-      if (b < batch) out[(b * s + i) * int64_t(s) + j] = from_f32<TOut>(v[q]);
+      for (int q = 0; q < kPack; ++q) {
+        const int64_t b = g * kPack + q;
+        if (b < batch) out[(b * s + i) * int64_t(s) + j] = from_f32<TOut>(v[q]);
+      }
+      continue;
+    }
+    float4* dst = epi.packed + g * int64_t(P) * P + int64_t(i + 1) * P + (j + 1);
+    if (epi.mode == kOutPacked) {
+      // narrowed through the storage precision like a user-visible result
+      *dst = make_float4(float(from_f32<TOut>(acc[r].x)), float(from_f32<TOut>(acc[r].y)),
+                         float(from_f32<TOut>(acc[r].z)), float(from_f32<TOut>(acc[r].w)));
+    } else {
+      // Landweber update x <- (-alpha) * grad + x in fp32 (solvers.cpp:139, tensor.cpp:338-343)
+      const float4 x = *dst;
+      const float na_ = epi.neg_alpha;
+      const float4 v = make_float4(__fadd_rn(__fmul_rn(na_, acc[r].x), x.x), __fadd_rn(__fmul_rn(na_, acc[r].y), x.y),
+                                   __fadd_rn(__fmul_rn(na_, acc[r].z), x.z), __fadd_rn(__fmul_rn(na_, acc[r].w), x.w));
+      *dst = v;
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < kPack; ++q)
+        if (g * kPack + q < batch && !isfinite(vv[q])) atomicMin(epi.flag, epi.iteration);  // all_finite, :140-142
     }
   }
 }
@@ -292,27 +413,40 @@ void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int
   RK_CUDA(cudaGetLastError());
 }
 
-void launch_forward(const Plan& p, const float4* packed_image, int64_t batch, int dtype, void* sino,
-                    cudaStream_t st) {
-  const int64_t n_rays = p.na * p.nd;
-  dim3 grid(blocks_for(n_rays, 256), unsigned(groups_of(batch)));
+void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st) {
+  const int P = int(s + 2);
+  dim3 grid(unsigned((P + 31) / 32), unsigned((P + 31) / 32), unsigned(groups_of(batch)));
+  KernelTimer timer(RK_KERNEL_PACK, st);
+  transpose_images_kernel<<<grid, dim3(32, 8), 0, st>>>(src, P, dst);
+  RK_CUDA(cudaGetLastError());
+}
+
+void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
+                    int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
+  const ForwardSchedule& F = p.fwd;
+  dim3 grid(unsigned(F.ctas_a * F.ctas_k), unsigned(groups_of(batch)));
+  const size_t smem = size_t(F.max_box) * sizeof(float4);
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
+    auto kern = forward_kernel<T>;
+    if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FORWARD, st);
-    forward_kernel<T><<<grid, 256, 0, st>>>(packed_image, int(p.s), p.ray_geom.as<float4>(),
-                                            p.ray_len.as<float2>(), n_rays, batch, static_cast<T*>(sino));
+    kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
+                                         p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int2>(),
+                                         int(p.na), int(p.nd), F.chunks, F.tbase, F.tlen, F.ctas_k, batch,
+                                         static_cast<T*>(sino), epi);
   });
   RK_CUDA(cudaGetLastError());
 }
 
 void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch, int dtype, void* image,
-                        cudaStream_t st) {
+                        cudaStream_t st, BpEpilogue epi) {
   const int tiles = int((p.s + kTile - 1) / kTile);
   dim3 grid(tiles, tiles, unsigned(groups_of(batch)));
   dim3 block(kTile, kTile / kRowsPerThread);
-  const size_t smem = size_t(p.bp_angle_chunk) * p.bp_window * sizeof(float4) +
-                      size_t(p.bp_angle_chunk) * (sizeof(AngleConst) + sizeof(int));
   const bool fan = p.g.kind == RK_FANBEAM;
+  const size_t smem = size_t(p.bp_angle_chunk) * p.bp_window * sizeof(float4) +
+                      size_t(p.bp_angle_chunk) * ((fan ? sizeof(FanConst) : sizeof(ParConst)) + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     auto kern = fan ? backproject_kernel<true, T> : backproject_kernel<false, T>;
@@ -320,7 +454,7 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
                                     p.g.source_distance, p.g.det_distance, p.trig.as<double2>(), p.bp_window,
-                                    p.bp_angle_chunk, batch, static_cast<T*>(image));
+                                    p.bp_angle_chunk, batch, static_cast<T*>(image), epi);
   });
   RK_CUDA(cudaGetLastError());
 }

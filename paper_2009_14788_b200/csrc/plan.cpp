@@ -95,44 +95,19 @@ inline bool clip_slab(double o, double d, double lo, double hi, double& t0, doub
   return true;
 }
 
-struct RaySetup {
-  float4 geom;  // px0, py0, hx, hy (padded pixel coordinates)
-  float2 len;   // h, n
-  int64_t n;
-};
-
 // The clip / sample-count / spacing prologue of integrate_ray
-// (projector.cpp:66-78), followed by the change of variables into padded
-// pixel coordinates used by bilinear (projector.cpp:48-49):
-//   px(m) = x(t_m) + s/2 - 0.5 (+1 border) = px0 + (m + 0.5) * hx
-//   py(m) = s/2 - y(t_m) - 0.5 (+1 border) = py0 + (m + 0.5) * hy
-// with t_m = t0 + (m + 0.5) * h.
-RaySetup setup_ray(int64_t s, double ox, double oy, double dx, double dy, double tmin, double tmax, double step) {
-  RaySetup r{};
+// (projector.cpp:66-78), kept in fp64 for the planners.
+RayD setup_ray(int64_t s, double ox, double oy, double dx, double dy, double tmin, double tmax, double step) {
+  RayD r{ox, oy, dx, dy, 0.0, 0.0, 0.0, 0};
   double half = 0.5 * double(s);
   double t0 = tmin, t1 = tmax;
   bool hit = clip_slab(ox, dx, -half, half, t0, t1) && clip_slab(oy, dy, -half, half, t0, t1) && (t1 > t0);
-  if (!hit) {
-    r.geom = make_float4(0.f, 0.f, 0.f, 0.f);
-    int zero = 0;
-    float zf;
-    std::memcpy(&zf, &zero, 4);
-    r.len = make_float2(0.f, zf);
-    r.n = 0;
-    return r;
-  }
+  if (!hit) return r;
   double len = t1 - t0;
-  int64_t n = std::max<int64_t>(1, int64_t(std::ceil(len / step)));
-  double h = len / double(n);
-  double ex = ox + t0 * dx, ey = oy + t0 * dy;  // clipped entry point
-  double px0 = ex + half + 0.5;                 // x + s/2 - 0.5, +1 border
-  double py0 = half - ey + 0.5;                 // s/2 - y - 0.5, +1 border
-  r.geom = make_float4(float(px0), float(py0), float(h * dx), float(-(h * dy)));
-  int ni = int(n);
-  float nf;
-  std::memcpy(&nf, &ni, 4);
-  r.len = make_float2(float(h), nf);
-  r.n = n;
+  r.n = std::max<int64_t>(1, int64_t(std::ceil(len / step)));
+  r.h = len / double(r.n);
+  r.t0 = t0;
+  r.t1 = t1;
   return r;
 }
 
@@ -158,8 +133,7 @@ void build_plan(Plan& p) {
   for (int64_t a = 0; a < na; ++a) trig[size_t(a)] = make_double2(std::cos(p.angles[size_t(a)]), std::sin(p.angles[size_t(a)]));
 
   // ----- forward ray table: forward_parallel_t / forward_fanbeam_t ray setup
-  std::vector<float4> rg(static_cast<size_t>(na * nd));
-  std::vector<float2> rl(static_cast<size_t>(na * nd));
+  std::vector<RayD> rays(static_cast<size_t>(na * nd));
   const double inf = std::numeric_limits<double>::infinity();
   int64_t total = 0;
   for (int64_t a = 0; a < na; ++a) {
@@ -168,7 +142,7 @@ void build_plan(Plan& p) {
     double sy = -g.source_distance * c;
     for (int64_t k = 0; k < nd; ++k) {
       double u = (double(k) - 0.5 * double(nd) + 0.5) * g.det_spacing;
-      RaySetup r;
+      RayD r;
       if (!fan) {
         // projector.cpp:107-109: origin u*(c, s), direction (-s, c), t unbounded
         r = setup_ray(s, u * c, u * sn, -sn, c, -inf, inf, g.step);
@@ -181,12 +155,14 @@ void build_plan(Plan& p) {
         r = setup_ray(s, sx, sy, dx / len, dy / len, 0.0, len, g.step);
       }
       if (r.n > (int64_t(1) << 30)) throw ValidationError("projector step too small: ray sample count overflows");
-      rg[size_t(a * nd + k)] = r.geom;
-      rl[size_t(a * nd + k)] = r.len;
+      rays[size_t(a * nd + k)] = r;
       total += r.n;
     }
   }
   p.forward_samples = total;
+  // per-ray records for the kernel + the chunk / box schedule (fwd_plan.cpp)
+  std::vector<float4> rg, ra;
+  build_forward_plan(p, rays, rg, ra);
 
   // ----- backprojection staging window: the widest detector footprint of a
   // 32x32 pixel tile over all tiles and angles (+ one cell on each side for
@@ -200,8 +176,9 @@ void build_plan(Plan& p) {
     double c = trig[size_t(a)].x, sn = trig[size_t(a)].y;
     for (int64_t ty = 0; ty < tiles; ++ty) {
       for (int64_t tx = 0; tx < tiles; ++tx) {
-        double x0 = double(tx * kBpTile) - half + 0.5, x1 = x0 + double(kBpTile - 1);
-        double y0 = half - double(ty * kBpTile) - 0.5, y1 = y0 - double(kBpTile - 1);
+        // in-image part of the tile (kernels.cu uses the same extent)
+        double x0 = double(tx * kBpTile) - half + 0.5, x1 = x0 + double(std::min<int64_t>(kBpTile, s - tx * kBpTile) - 1);
+        double y0 = half - double(ty * kBpTile) - 0.5, y1 = y0 - double(std::min<int64_t>(kBpTile, s - ty * kBpTile) - 1);
         double lo = inf, hi = -inf;
         for (double x : {x0, x1})
           for (double y : {y0, y1}) {
@@ -215,8 +192,12 @@ void build_plan(Plan& p) {
             lo = std::min(lo, kf);
             hi = std::max(hi, kf);
           }
-        int64_t w = int64_t(std::floor(hi)) - int64_t(std::floor(lo)) + 3;
-        need = std::max(need, w);
+        // window [floor(lo) - 1, floor(hi) + 2] clipped to [-2, nd + 1]: beyond
+        // that every tap is outside the detector (zero), and the kernel's
+        // clamp lands on the two zero cells at the clipped end
+        int64_t ws = std::max<int64_t>(int64_t(std::floor(lo)) - 1, -2);
+        int64_t we = std::min<int64_t>(int64_t(std::floor(hi)) + 2, nd + 1);
+        need = std::max(need, we - ws + 1);
       }
       if (!fan) break;  // parallel: footprint width is translation invariant up to floor effects
     }
@@ -224,11 +205,11 @@ void build_plan(Plan& p) {
   if (!fan) need += 1;  // floor effects across tiles
   need += 1;            // rounding margin
   int64_t window = (need + 3) / 4 * 4;
-  if (window > 4096)
-    throw ValidationError("backprojection footprint of " + std::to_string(window) +
-                          " detector cells per 32x32 tile is too wide (source too close to the image)");
+  if (window > 12 * 1024)
+    throw ValidationError("backprojection window of " + std::to_string(window) +
+                          " detector cells exceeds shared memory (det_count too large)");
   p.bp_window = int(window);
-  // angles per staging pass: keep the window slab near 32 KB
+  // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to 192 KB)
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(32, (32 * 1024) / (window * 16)));
   p.bp_angle_chunk = int(chunk);
 
@@ -236,10 +217,14 @@ void build_plan(Plan& p) {
   if (p.device < 0) return;
   RK_CUDA(cudaSetDevice(p.device));
   p.ray_geom.reserve(rg.size() * sizeof(float4));
-  p.ray_len.reserve(rl.size() * sizeof(float2));
+  p.ray_aux.reserve(ra.size() * sizeof(float4));
   p.trig.reserve(trig.size() * sizeof(double2));
   RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(p.ray_len.ptr, rl.data(), rl.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(p.ray_aux.ptr, ra.data(), ra.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  p.fwd_boxes.reserve(p.fwd.boxes.size() * sizeof(int4));
+  p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int2));
+  RK_CUDA(cudaMemcpy(p.fwd_boxes.ptr, p.fwd.boxes.data(), p.fwd.boxes.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaEventCreateWithFlags(&p.scratch_free, cudaEventDisableTiming));
 }

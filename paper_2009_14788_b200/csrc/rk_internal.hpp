@@ -62,7 +62,32 @@ constexpr int kPack = 4;
 
 inline int64_t groups_of(int64_t batch) { return (batch + kPack - 1) / kPack; }
 
+// ----------------------------------------------------------------- forward schedule
+// fp64 ray after the reference's clip prologue (projector.cpp:66-78)
+struct RayD {
+  double ox, oy, dx, dy;  // origin and unit direction (world coordinates)
+  double t0, t1, h;       // clipped parameter range and sample spacing
+  int64_t n;              // samples (0: the ray misses the image)
+};
+
+struct ForwardSchedule {
+  int A = 8;        // angles per CTA (one warp each)
+  int W = 32;       // detectors per CTA (one lane each)
+  float tbase = 0;  // t of the first chunk boundary
+  float tlen = 0;   // chunk length along the ray (world units)
+  int chunks = 0;
+  int ctas_a = 0, ctas_k = 0;
+  int64_t max_box = 0;  // largest rows * pitch over all boxes (float4 cells)
+  bool any_transposed = false;
+  std::vector<int4> boxes;  // ctas * chunks
+  std::vector<int2> cta;    // ctas
+};
+
 // ----------------------------------------------------------------- plan
+struct Plan;
+void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<float4>& ray_geom,
+                        std::vector<float4>& ray_aux);
+
 struct Plan {
   int device = 0;
   rk_geometry g{};              // resolved; g.angles -> angles.data()
@@ -72,7 +97,13 @@ struct Plan {
 
   // forward: one record per ray (a * nd + k), built in fp64 on the host
   DeviceBuffer ray_geom;   // float4 {px0, py0, hx, hy} in padded pixel coordinates
-  DeviceBuffer ray_len;    // float2 {h, n (int bits)}
+  DeviceBuffer ray_aux;    // float4 {h, n (int bits), t0, 1/h}
+  // forward schedule (fwd_plan.cpp): CTA = A angles x W detectors; the rays
+  // are marched chunk by chunk along t, each chunk's image footprint (box) is
+  // staged in shared memory
+  ForwardSchedule fwd;
+  DeviceBuffer fwd_boxes;  // int4 {row0, col0, rows, cols} per (cta, chunk), staged-image coordinates
+  DeviceBuffer fwd_cta;    // int2 {pitch, transposed} per cta
   // backprojection: per-angle trig in fp64
   DeviceBuffer trig;       // double2 {cos, sin}
   int bp_window = 0;       // staged detector cells per (tile, angle)
@@ -80,11 +111,11 @@ struct Plan {
 
   // scratch (serialised by `mu`; `scratch_free` orders reuse across streams)
   std::mutex mu;
-  DeviceBuffer packed_image, packed_sino;
+  DeviceBuffer packed_image, packed_image_t, packed_sino;
   cudaEvent_t scratch_free = nullptr;
   // host-buffer (*_host) pipelines: two streams, each with its own buffers
   cudaStream_t copy_streams[2] = {nullptr, nullptr};
-  DeviceBuffer pipe_in[2], pipe_out[2], pipe_pk[2];
+  DeviceBuffer pipe_in[2], pipe_out[2], pipe_pk[2], pipe_pkt[2];
   // solver scratch
   DeviceBuffer solver_a, solver_b, solver_c, solver_d, solver_scalars;
 
@@ -115,10 +146,31 @@ int filter_kind_from_name(const std::string& name);
 void launch_pack_images(int dtype, const void* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
 void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int64_t nd, float4* dst,
                       cudaStream_t st);
-void launch_forward(const Plan& p, const float4* packed_image, int64_t batch, int dtype, void* sino,
-                    cudaStream_t st);
+// Kernel epilogues.  kOutUser: user layout in the storage dtype (the default
+// reference-shaped result); kOutPacked: packed float4 layout (values narrowed
+// through the dtype first); forward kOutResidual: packed (A x - y); backprojection
+// kOutAxpy: packed x <- (-alpha) * (A' r) + x with a non-finite flag.
+enum { kOutUser = 0, kOutPacked = 1, kOutResidual = 2, kOutAxpy = 3 };
+struct FwdEpilogue {
+  int mode = kOutUser;
+  float4* packed = nullptr;       // [G][na][nd]
+  const float4* resid = nullptr;  // y for kOutResidual, same layout
+};
+struct BpEpilogue {
+  int mode = kOutUser;
+  float4* packed = nullptr;  // [G][s+2][s+2] (interior written)
+  float neg_alpha = 0.f;     // kOutAxpy
+  int* flag = nullptr;       // kOutAxpy: atomicMin(iteration) on a non-finite iterate
+  int iteration = 0;
+};
+
+// packed image -> its transpose ([G][s+2][s+2], rows <-> columns)
+void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
+// packed_image_t is only read when the schedule has transposed CTAs
+void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
+                    int dtype, void* sino, cudaStream_t st, FwdEpilogue epi = FwdEpilogue{});
 void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch, int dtype, void* image,
-                        cudaStream_t st);
+                        cudaStream_t st, BpEpilogue epi = BpEpilogue{});
 // filter: rows of det_count in `dtype`; writes either the user layout
 // (`out`, dtype) or, when `packed_out` is set, the packed sino layout.
 void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, int64_t n_angles, void* out,
