@@ -384,18 +384,57 @@ int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino,
   });
 }
 
+// solvers.cpp:111-128
 int rk_estimate_alpha(rk_plan* plan, int iterations, uint64_t seed, double* alpha) {
-  return guarded([&] { throw rk::ValidationError("rk_estimate_alpha: not built yet"); });
+  return guarded([&] {
+    check_device_plan(plan);
+    require(alpha != nullptr, "alpha pointer is null");
+    rk::Plan& p = plan->p;
+    cudaStream_t st = nullptr;
+    ScratchLease lease(p, st);
+    *alpha = rk::run_estimate_alpha(p, iterations, seed, st);
+  });
 }
 
+// solvers.cpp:130-145
 int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, double alpha,
                  int iterations, void* d_x, int* failed_iteration, void* stream) {
-  return guarded([&] { throw rk::ValidationError("rk_landweber: not built yet"); });
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_y != nullptr && d_guess != nullptr && d_x != nullptr, "landweber pointer is null");
+    rk::Plan& p = plan->p;
+    int failed = -1;
+    {
+      ScratchLease lease(p, as_stream(stream));
+      failed = rk::run_landweber(p, dtype, d_y, d_guess, batch, alpha, iterations, d_x, as_stream(stream));
+    }
+    if (failed_iteration) *failed_iteration = failed;
+    if (failed >= 0)
+      throw rk::NumericalError("landweber produced a non-finite iterate at iteration " + std::to_string(failed),
+                               failed);
+  });
 }
 
+// solvers.cpp:162-166 (cg_impl :47-107)
 int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter,
             double tolerance, void* d_x, int* failed_iteration, void* stream) {
-  return guarded([&] { throw rk::ValidationError("rk_cgne: not built yet"); });
+  return guarded([&] {
+    check_device_plan(plan);
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_y != nullptr && d_guess != nullptr && d_x != nullptr, "cgne pointer is null");
+    rk::Plan& p = plan->p;
+    int failed = -1;
+    {
+      ScratchLease lease(p, as_stream(stream));
+      failed = rk::run_cgne(p, dtype, d_y, d_guess, batch, max_iter, tolerance, d_x, as_stream(stream));
+    }
+    if (failed_iteration) *failed_iteration = failed;
+    if (failed >= 0)
+      throw rk::NumericalError("cg: curvature p'Ap is not positive at iteration " + std::to_string(failed), failed);
+  });
 }
 
 int rk_profiling_enable(int enable) {

@@ -102,18 +102,30 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     ray_aux[r] = make_float4(float(R.h), nf, float(R.t0), float(1.0 / R.h));
   }
 
-  // ---- chunking along t
+  // ---- CTA angle sets: angles sorted by direction (mod 2 pi: theta and theta + pi
+  // march the same lines in opposite t), A_eff consecutive ones per CTA (the
+  // reference accepts arbitrary angle lists, geometry.cpp:12-18)
   ForwardSchedule& F = p.fwd;
   F.A = 8;
   F.W = 32;
+  std::vector<int> order(static_cast<size_t>(na));
+  for (int64_t a = 0; a < na; ++a) order[size_t(a)] = int(a);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    const double tx = std::fmod(std::fmod(p.angles[size_t(x)], 2.0 * M_PI) + 2.0 * M_PI, 2.0 * M_PI);
+    const double ty = std::fmod(std::fmod(p.angles[size_t(y)], 2.0 * M_PI) + 2.0 * M_PI, 2.0 * M_PI);
+    return tx < ty;
+  });
   const double R = half * std::sqrt(2.0);  // every image point lies within R of the centre
   const double t_lo = (fan ? p.g.source_distance : 0.0) - R - 1.0;
   const double t_hi = (fan ? p.g.source_distance : 0.0) + R + 1.0;
-  F.ctas_a = int((na + F.A - 1) / F.A);
   F.ctas_k = int((nd + F.W - 1) / F.W);
-  const int ctas = F.ctas_a * F.ctas_k;
   const int64_t box_budget = 6 * 1024;  // float4 cells (96 KB)
 
+  for (int a_eff : {8, 4, 2, 1}) {
+  F.ctas_a = int((na + a_eff - 1) / a_eff);
+  const int ctas = F.ctas_a * F.ctas_k;
+  F.slots.assign(size_t(F.ctas_a) * F.A, -1);
+  for (int64_t i = 0; i < na; ++i) F.slots[size_t((i / a_eff) * F.A + (i % a_eff))] = order[size_t(i)];
   for (double tlen : {32.0, 24.0, 16.0, 12.0, 8.0, 6.0, 4.0}) {
     F.tlen = float(tlen);
     F.tbase = float(t_lo);
@@ -134,8 +146,8 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           const double tb = double(F.tbase) + double(c + 1) * tlen + 1.0;
           double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
           for (int ai = 0; ai < F.A; ++ai) {
-            const int64_t a = int64_t(ca) * F.A + ai;
-            if (a >= na) break;
+            const int a = F.slots[size_t(ca) * F.A + ai];
+            if (a < 0) continue;
             for (int ki = 0; ki < F.W; ++ki) {
               const int64_t k = int64_t(ck) * F.W + ki;
               if (k >= nd) break;
@@ -167,11 +179,11 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
         for (int st = 0; st < steps; ++st) {
           const double tt = t_lo + (t_hi - t_lo) * (0.2 + 0.6 * double(st) / double(steps - 1));
           for (int ai = 0; ai < F.A; ++ai) {
-            const int64_t a = int64_t(ca) * F.A + ai;
+            const int a = F.slots[size_t(ca) * F.A + ai];
             for (int ki = 0; ki < F.W; ++ki) {
               const int64_t k = int64_t(ck) * F.W + ki;
               Pt q{NAN, NAN};
-              if (a < na && k < nd) {
+              if (a >= 0 && k < nd) {
                 const RayD& ry = rays[size_t(a * nd + k)];
                 if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
                   // the sample the lane reaches when the chunk-aligned march is at tt
@@ -226,14 +238,16 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           if (b.z) ++boxes, cells += int64_t(b.z) * b.w;
         for (const int2& c : F.cta) ntr += c.y;
         std::fprintf(stderr,
-                     "[rk] forward schedule: tlen %.0f, %d chunks, %d CTAs (%lld transposed), %lld boxes, "
-                     "mean box %.0f texels, max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
-                     double(F.tlen), F.chunks, ctas, (long long)ntr, (long long)boxes,
+                     "[rk] forward schedule: %d angles/CTA, tlen %.0f, %d chunks, %d CTAs (%lld transposed), "
+                     "%lld boxes, mean box %.0f texels, max box %lld cells (%.1f KB), staged texels per image "
+                     "%.2fM\n",
+                     a_eff, double(F.tlen), F.chunks, ctas, (long long)ntr, (long long)boxes,
                      boxes ? double(cells) / double(boxes) : 0.0, (long long)F.max_box,
                      double(F.max_box) * 16.0 / 1024.0, double(cells) / 1e6);
       }
       return;
     }
+  }
   }
   throw ValidationError("forward schedule: no chunk length keeps the staged image box within shared memory");
 }

@@ -129,16 +129,16 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 template <class TOut>
 __global__ void __launch_bounds__(kFwdThreads, 2) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
-    const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int2* __restrict__ cta_cfg, int na,
-    int nd, int chunks, float tbase, float tlen, int ctas_k, int64_t batch, TOut* __restrict__ sino,
-    FwdEpilogue epi) {
+    const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int2* __restrict__ cta_cfg,
+    const int* __restrict__ slots, int na, int nd, int chunks, float tbase, float tlen, int ctas_k, int64_t batch,
+    TOut* __restrict__ sino, FwdEpilogue epi) {
   extern __shared__ float4 box_s[];
   const int cta = blockIdx.x;
   const int ga = cta / ctas_k, gk = cta - ga * ctas_k;
   const int64_t g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a = ga * (kFwdThreads / 32) + warp, k = gk * 32 + lane;
-  const bool valid = a < na && k < nd;
+  const int a = __ldg(slots + ga * (kFwdThreads / 32) + warp), k = gk * 32 + lane;  // angles sorted by direction
+  const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
   const int2 cfg = cta_cfg[cta];
   const int pitch = cfg.x;
@@ -433,7 +433,7 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
     KernelTimer timer(RK_KERNEL_FORWARD, st);
     kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
                                          p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int2>(),
-                                         int(p.na), int(p.nd), F.chunks, F.tbase, F.tlen, F.ctas_k, batch,
+                                         p.fwd_slots.as<int>(), int(p.na), int(p.nd), F.chunks, F.tbase, F.tlen, F.ctas_k, batch,
                                          static_cast<T*>(sino), epi);
   });
   RK_CUDA(cudaGetLastError());

@@ -225,6 +225,8 @@ void build_plan(Plan& p) {
   p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int2));
   RK_CUDA(cudaMemcpy(p.fwd_boxes.ptr, p.fwd.boxes.data(), p.fwd.boxes.size() * sizeof(int4), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  p.fwd_slots.reserve(p.fwd.slots.size() * sizeof(int));
+  RK_CUDA(cudaMemcpy(p.fwd_slots.ptr, p.fwd.slots.data(), p.fwd.slots.size() * sizeof(int), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaEventCreateWithFlags(&p.scratch_free, cudaEventDisableTiming));
 }

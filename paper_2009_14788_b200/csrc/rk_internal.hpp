@@ -81,6 +81,7 @@ struct ForwardSchedule {
   bool any_transposed = false;
   std::vector<int4> boxes;  // ctas * chunks
   std::vector<int2> cta;    // ctas
+  std::vector<int> slots;   // ctas_a * A angle indices (-1: idle warp)
 };
 
 // ----------------------------------------------------------------- plan
@@ -104,6 +105,7 @@ struct Plan {
   ForwardSchedule fwd;
   DeviceBuffer fwd_boxes;  // int4 {row0, col0, rows, cols} per (cta, chunk), staged-image coordinates
   DeviceBuffer fwd_cta;    // int2 {pitch, transposed} per cta
+  DeviceBuffer fwd_slots;  // int angle index per (cta row, warp), -1 = idle
   // backprojection: per-angle trig in fp64
   DeviceBuffer trig;       // double2 {cos, sin}
   int bp_window = 0;       // staged detector cells per (tile, angle)
@@ -177,6 +179,15 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
                    float4* packed_out, cudaStream_t st);
 
 size_t dtype_size(int dtype);
+
+// ----------------------------------------------------------------- solvers (solver.cu)
+void unpack_images(int dtype, const float4* src, int64_t batch, int64_t s, void* dst, cudaStream_t st);
+// return the first failing iteration (DivergenceError / NotPositiveDefiniteError) or -1
+int run_landweber(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, double alpha,
+                  int iterations, void* d_x, cudaStream_t st);
+int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter, double tol,
+             void* d_x, cudaStream_t st);
+double run_estimate_alpha(Plan& p, int iterations, uint64_t seed, cudaStream_t st);
 
 // ----------------------------------------------------------------- instrumentation (profiling.cu)
 constexpr int kKernelKinds = RK_KERNEL_KINDS;

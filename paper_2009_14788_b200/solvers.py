@@ -21,7 +21,7 @@ from .projector import get_plan
 from .rng import Rng
 
 
-_FUSED = False  # flipped on once the fused rk_landweber / rk_cgne / rk_estimate_alpha kernels land
+_FUSED = True  # fused device solvers of the C ABI (set False to run the generic torch loop)
 
 
 def _fused_ok(op: LinearOperator) -> bool:
