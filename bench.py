@@ -55,13 +55,6 @@ def env_int(name, default):
         return default
 
 
-def shard(batch, world, rank):
-    """Contiguous shard of ceil(batch / world) elements."""
-    per = -(-batch // world)
-    lo = min(batch, rank * per)
-    return lo, min(batch, lo + per)
-
-
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -235,7 +228,9 @@ def main():
     k, s, na, stop, nd, src, B = WORKLOADS[args.workload]
     ang = rk.angles_linspace(0.0, stop, na)
     g = rk.make_parallel(s, ang, nd) if k == "parallel" else rk.make_fanbeam(s, ang, src, det_count=nd)
-    lo, hi = shard(B, world, rank)
+    from paper_2009_14788_b200.sharding import shard_range
+
+    lo, hi = shard_range(B, world, rank)  # contiguous batch shard, no data-path collective
     nb = hi - lo
 
     # synthetic inputs: phantom x (e+1)/128, Rng(seed=e) uniform for odd e
