@@ -39,12 +39,16 @@ inline Pt to_pixel(double x, double y, double half) { return {x + half + 0.5, ha
 
 // Bank-conflict cost of one orientation / pitch: sum over quarter warps and
 // taps of the number of distinct 16-byte cells that share a slot (1 = free).
-double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, bool transposed, int pitch) {
+// swap: 0 none, 1 odd lanes load the bottom row first, 2 odd lanes load the
+// right column first (kernel: which tap each lane issues in each of its four
+// 128-bit loads; spreads the quarter warp over more bank slots).
+double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, bool transposed, int pitch, int swap) {
   double cost = 0.0;
   const int nw = int(lanes_at_step.size()) / lanes_per_warp;
   for (int w = 0; w < nw; ++w) {
     for (int q = 0; q < lanes_per_warp; q += 8) {
       int64_t bi[8], bj[8];
+      int lane_of[8];
       int used = 0;
       for (int l = 0; l < 8 && q + l < lanes_per_warp; ++l) {
         const Pt& pt = lanes_at_step[size_t(w * lanes_per_warp + q + l)];
@@ -52,6 +56,7 @@ double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, b
         const double cx = transposed ? pt.py : pt.px, cy = transposed ? pt.px : pt.py;
         bj[used] = int64_t(std::floor(cx));
         bi[used] = int64_t(std::floor(cy));
+        lane_of[used] = q + l;
         ++used;
       }
       for (int tap = 0; tap < 4; ++tap) {
@@ -59,7 +64,10 @@ double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, b
         int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int worst = used ? 1 : 0;
         for (int u = 0; u < used; ++u) {
-          addr[u] = (bi[u] + (tap >> 1)) * pitch + bj[u] + (tap & 1);
+          const bool odd = (lane_of[u] & 1) != 0;
+          const int dy = (swap == 1 && odd) ? 1 - (tap >> 1) : (tap >> 1);
+          const int dx = (swap == 2 && odd) ? 1 - (tap & 1) : (tap & 1);
+          addr[u] = (bi[u] + dy) * pitch + bj[u] + dx;
           bool dup = false;
           for (int v = 0; v < u && !dup; ++v) dup = addr[v] == addr[u];
           if (!dup) worst = std::max(worst, ++cnt[int(((addr[u] % 8) + 8) % 8)]);
@@ -197,20 +205,25 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           }
         }
         double best = 1e300;
-        int best_pitch = int(maxcols[0]), best_tr = 0;
+        int best_pitch = int(maxcols[0]), best_tr = 0, best_swap = 0;
         for (int tr = 0; tr < 2; ++tr) {
           if (maxcols[tr] == 0) continue;
-          for (int d = 0; d < 8; ++d) {
-            const int pitch = int(maxcols[tr]) + d;
-            const double cst = conflict_cost(sim, F.W, tr == 1, pitch) * (1.0 + 1e-4 * d + 1e-3 * tr);
-            if (cst < best) {
-              best = cst;
-              best_pitch = pitch;
-              best_tr = tr;
+          for (int swap = 0; swap < 3; ++swap) {
+            for (int d = 0; d < 8; ++d) {
+              const int pitch = int(maxcols[tr]) + d;
+              const double cst =
+                  conflict_cost(sim, F.W, tr == 1, pitch, swap) * (1.0 + 1e-4 * d + 1e-3 * tr + 1e-5 * swap);
+              if (cst < best) {
+                best = cst;
+                best_pitch = pitch;
+                best_tr = tr;
+                best_swap = swap;
+              }
             }
           }
         }
-        F.cta[size_t(cta)] = make_int2(best_pitch, best_tr);
+        // cfg.y: bit 0 transposed image, bits 1-2 per-lane tap order
+        F.cta[size_t(cta)] = make_int2(best_pitch, best_tr | (best_swap << 1));
         for (int c = 0; c < F.chunks; ++c) {
           int4 b = bx[size_t(c)];
           if (b.z == 0) continue;
@@ -230,13 +243,13 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     }
     for (auto& th : pool) th.join();
     for (int64_t v : mb) F.max_box = std::max(F.max_box, v);
-    for (const int2& c : F.cta) F.any_transposed |= c.y == 1;
+    for (const int2& c : F.cta) F.any_transposed |= (c.y & 1) == 1;
     if (F.max_box <= box_budget) {
       if (std::getenv("RK_DEBUG_PLAN")) {
         int64_t boxes = 0, cells = 0, ntr = 0;
         for (const int4& b : F.boxes)
           if (b.z) ++boxes, cells += int64_t(b.z) * b.w;
-        for (const int2& c : F.cta) ntr += c.y;
+        for (const int2& c : F.cta) ntr += c.y & 1;
         std::fprintf(stderr,
                      "[rk] forward schedule: %d angles/CTA, tlen %.0f, %d chunks, %d CTAs (%lld transposed), "
                      "%lld boxes, mean box %.0f texels, max box %lld cells (%.1f KB), staged texels per image "

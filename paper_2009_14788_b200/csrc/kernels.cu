@@ -127,7 +127,7 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // outside its box.  CTAs whose lanes spread mostly along image columns read
 // the transposed packed image with x and y swapped (bilinear is symmetric).
 template <class TOut>
-__global__ void __launch_bounds__(kFwdThreads, 2) forward_kernel(
+__global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int2* __restrict__ cta_cfg,
     const int* __restrict__ slots, int na, int nd, int chunks, float tbase, float tlen, int ctas_k, int64_t batch,
@@ -142,7 +142,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2) forward_kernel(
   const int64_t r = int64_t(a) * nd + k;
   const int2 cfg = cta_cfg[cta];
   const int pitch = cfg.x;
-  const bool tr = cfg.y != 0;
+  const bool tr = (cfg.y & 1) != 0;
+  // Per-lane tap order chosen by the planner against bank conflicts: odd lanes
+  // issue the bottom row first (swap 1) or the right column first (swap 2).
+  // Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA) (rowB,colB); the
+  // weights follow the same order, so no value is moved between registers.
+  const int swap = (cfg.y >> 1) & 3;
+  const bool odd = (threadIdx.x & 1) != 0;
+  const bool rs = swap == 1 && odd, cs = swap == 2 && odd;
+  const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
+  const int dX = cs ? -1 : 1;
+  const int dY = rs ? -pitch : pitch;
   float4 G = make_float4(0.f, 0.f, 0.f, 0.f), X = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     G = __ldg(ray_geom + r);
@@ -184,14 +194,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2) forward_kernel(
       const float fx = px - fj, fy = py - fi;
       const int j = min(max(int(fj), 0), jmax);
       const int i = min(max(int(fi), 0), imax);
-      const float4* q = box_s + i * pitch + j;
-      const float4 v00 = q[0], v01 = q[1], v10 = q[pitch], v11 = q[pitch + 1];
+      const float4* q = box_s + (i * pitch + j + dA);
+      const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
       const float gx = 1.f - fx, gy = 1.f - fy;
-      const float w00 = gx * gy, w01 = fx * gy, w10 = gx * fy, w11 = fx * fy;
-      a0 = fmaf(w00, v00.x, fmaf(w01, v01.x, fmaf(w10, v10.x, fmaf(w11, v11.x, a0))));
-      a1 = fmaf(w00, v00.y, fmaf(w01, v01.y, fmaf(w10, v10.y, fmaf(w11, v11.y, a1))));
-      a2 = fmaf(w00, v00.z, fmaf(w01, v01.z, fmaf(w10, v10.z, fmaf(w11, v11.z, a2))));
-      a3 = fmaf(w00, v00.w, fmaf(w01, v01.w, fmaf(w10, v10.w, fmaf(w11, v11.w, a3))));
+      const float ya = rs ? fy : gy, yb = rs ? gy : fy;
+      const float xa = cs ? fx : gx, xb = cs ? gx : fx;
+      const float w1 = xa * ya, w2 = xb * ya, w3 = xa * yb, w4 = xb * yb;
+      a0 = fmaf(w1, v1.x, fmaf(w2, v2.x, fmaf(w3, v3.x, fmaf(w4, v4.x, a0))));
+      a1 = fmaf(w1, v1.y, fmaf(w2, v2.y, fmaf(w3, v3.y, fmaf(w4, v4.y, a1))));
+      a2 = fmaf(w1, v1.z, fmaf(w2, v2.z, fmaf(w3, v3.z, fmaf(w4, v4.z, a2))));
+      a3 = fmaf(w1, v1.w, fmaf(w2, v2.w, fmaf(w3, v3.w, fmaf(w4, v4.w, a3))));
     }
   }
   if (!valid) return;
