@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--workload", default="par512", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config 3/4/5 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -212,7 +213,6 @@ def main():
 
     import paper_2009_14788_b200 as rk
     from paper_2009_14788_b200 import _lib
-    from oracle import batched_phantom  # noqa: F401  (input generator only)
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -354,6 +354,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_images_per_s(args.workload)
+    extras = None
+    if world == 1 and not args.no_extras:
+        del x, sino, out, flush
+        torch.cuda.empty_cache()
+        extras = measure_extras(rk, _lib, dev)
 
     if rank == 0:
         line = {
@@ -365,7 +370,7 @@ def main():
                        "global_batch": B, "per_gpu_batch": nb, "parallelism": f"batch-shard x{world}, no collective",
                        "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kern,
-            "clocks": clk,
+            "clocks": clk, "other_configs": extras,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -373,11 +378,90 @@ def main():
     return 0
 
 
-def rk_phantom(s):
-    """Modified Shepp-Logan via the oracle port (input generation only, not timed)."""
-    from oracle import PortOracle
+_SL = [(1.0, 0.69, 0.92, 0.0, 0.0, 0.0), (-0.8, 0.6624, 0.874, 0.0, -0.0184, 0.0),
+       (-0.2, 0.11, 0.31, 0.22, 0.0, -18.0), (-0.2, 0.16, 0.41, -0.22, 0.0, 18.0),
+       (0.1, 0.21, 0.25, 0.0, 0.35, 0.0), (0.1, 0.046, 0.046, 0.0, 0.1, 0.0), (0.1, 0.046, 0.046, 0.0, -0.1, 0.0),
+       (0.1, 0.046, 0.023, -0.08, -0.605, 0.0), (0.1, 0.023, 0.023, 0.0, -0.606, 0.0),
+       (0.1, 0.023, 0.046, 0.06, -0.605, 0.0)]
 
-    return PortOracle().shepp_logan(s)[0]
+
+def rk_phantom(s):
+    """Synthetic input: modified Shepp-Logan (the reference's table, phantom.cpp:18-29)
+    rasterised at 400^2 and bilinearly resampled to s^2 (phantom.cpp:61-101), numpy."""
+    base = 400
+    y = (base - 1 - 2 * np.arange(base))[:, None] / base
+    x = (2 * np.arange(base) + 1 - base)[None, :] / base
+    img = np.zeros((base, base))
+    for v, a, b, x0, y0, th in _SL:
+        t = np.deg2rad(th)
+        u = (x - x0) * np.cos(t) + (y - y0) * np.sin(t)
+        w = -(x - x0) * np.sin(t) + (y - y0) * np.cos(t)
+        img += v * ((u * u) / (a * a) + (w * w) / (b * b) <= 1.0)
+    c = ((2 * np.arange(s) + 1) * base - s) / (2.0 * s)
+    i0 = np.clip(np.floor(c).astype(int), 0, base - 1)
+    f = np.where((c < 0) | (i0 >= base - 1), 0.0, c - np.floor(c))
+    i1 = np.minimum(i0 + 1, base - 1)
+    top = (1 - f)[None, :] * img[i0][:, i0] + f[None, :] * img[i0][:, i1]
+    bot = (1 - f)[None, :] * img[i1][:, i0] + f[None, :] * img[i1][:, i1]
+    return ((1 - f)[:, None] * top + f[:, None] * bot).astype(np.float32)
+
+
+def measure_extras(rk, _lib, dev):
+    """Device-timed numbers for the other BASELINE configs (N=1 only; 1 warm-up + 3 runs each)."""
+    import torch
+
+    out = {}
+    st = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn, runs=3):
+        fn()
+        torch.cuda.synchronize(dev)
+        tot = 0.0
+        for i in range(runs):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            torch.cuda.synchronize(dev)
+            tot += a.elapsed_time(b)
+        return tot / runs
+
+    # config 3: fan-beam 512^2, 512 angles over 2 pi, D_so = D_dd = 512, batch 128, fp32
+    gf = rk.make_fanbeam(512, rk.angles_linspace(0.0, 2 * math.pi, 512), 512.0)
+    x = torch.from_numpy(np.stack([rk_phantom(512) * ((e + 1) / 128.0) for e in range(128)])).to(dev)
+    y = rk.forward(gf, x)
+    ms = timed(lambda: rk.backprojection(gf, rk.forward(gf, x)))
+    out["cfg3_fan512_b128_fp32"] = {"metric": "forward+backprojection images/s", "value": 128 / (ms * 1e-3),
+                                    "ms": ms}
+    del x, y
+    # config 4: FBP 1024^2, 720 angles, nd 1024 and 1449, batch 64, fp32 and fp16 storage
+    ph = rk_phantom(1024)
+    x = torch.from_numpy(np.stack([ph * ((e + 1) / 64.0) for e in range(64)])).to(dev)
+    for nd in (1024, 1449):
+        g4 = rk.make_parallel(1024, rk.angles_linspace(0.0, math.pi, 720), nd)
+        sino = rk.forward(g4, x)
+        for dt, name in ((torch.float32, "fp32"), (torch.float16, "fp16")):
+            s_ = sino.to(dt)
+            ms = timed(lambda: rk.fbp(g4, s_))
+            out[f"cfg4_fbp1024_720_nd{nd}_b64_{name}"] = {"metric": "FBP images/s", "value": 64 / (ms * 1e-3), "ms": ms}
+        del sino
+    del x
+    # config 5: 50 Landweber / CGNE iterations, 512^2, 256 angles, batch 256 (the whole 8-GPU batch on one GPU)
+    g5 = rk.make_parallel(512, rk.angles_linspace(0.0, math.pi, 256))
+    op = rk.projector_operator(g5)
+    x = torch.from_numpy(np.stack([rk_phantom(512) * ((e + 1) / 256.0) for e in range(256)])).to(dev)
+    y = rk.forward(g5, x)
+    z = torch.zeros_like(x)
+    alpha = 0.95 * rk.estimate_alpha(op, 20, 0)
+    ms = timed(lambda: rk.landweber(op, y, z, alpha, 50), runs=1)
+    out["cfg5_landweber50_512_256_b256"] = {"metric": "reconstructed images/s (50 iterations)",
+                                            "value": 256 / (ms * 1e-3), "ms": ms, "alpha": alpha}
+    ms = timed(lambda: rk.cgne(op, z, y, 50), runs=1)
+    out["cfg5_cgne50_512_256_b256"] = {"metric": "reconstructed images/s (50 iterations)", "value": 256 / (ms * 1e-3),
+                                       "ms": ms}
+    return out
 
 
 def ctypes_void(p):
