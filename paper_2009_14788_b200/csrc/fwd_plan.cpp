@@ -1,22 +1,29 @@
 // Forward-projection schedule (host, fp64).
 //
-// The forward kernel (kernels.cu) gives each CTA a block of A consecutive
-// angles x W consecutive detector cells (one warp per angle, one lane per
-// ray) and marches all of its rays together, chunk by chunk, along the ray
-// parameter t (reference: t_m = t0 + (m + 0.5) h, projector.cpp:75-81).
-// Before each chunk the CTA stages into shared memory the axis-aligned box of
-// packed image texels (4 images per 16-byte texel) that the chunk's samples
-// can touch; every bilinear tap (projector.cpp:47-64) is then a 128-bit
-// shared-memory load.  This file computes, per CTA:
-//   * the box of every chunk, from the exact fp64 ray segments, with one
-//     unit of slack in t and one texel of slack around the taps (the kernel
-//     assigns samples to chunks in fp32);
-//   * the shared-memory orientation and row pitch: the 8 lanes of a quarter
-//     warp read 8 neighbouring rays at one sample step, i.e. 8 texels along
-//     a digital line; the planner simulates the bank slots of those
-//     addresses for both orientations (the transposed copy of the packed
-//     image serves the "mostly vertical" lanes) and every pitch residue mod 8
-//     and keeps the cheapest.
+// The forward kernel (kernels.cu) gives each CTA 8 warps; warp w marches 32
+// consecutive detector cells of one angle (one lane per ray).  Angles are
+// sorted by direction (mod 2 pi: theta and theta + pi march the same lines in
+// opposite t; the reference accepts arbitrary angle lists,
+// geometry.cpp:12-18), and a CTA takes `aa` consecutive sorted angles x `db`
+// consecutive 32-cell blocks (aa * db = 8).  All rays of a CTA march together
+// along the ray parameter t (reference: t_m = t0 + (m + 0.5) h,
+// projector.cpp:75-81), chunk by chunk.  Before each chunk the CTA stages into
+// shared memory the axis-aligned box of packed image texels (4 images per
+// 16-byte texel) that the chunk's samples can touch; every bilinear tap
+// (projector.cpp:47-64) is then a 128-bit shared-memory load.
+//
+// Per CTA this file decides
+//   * the shared-memory layout: the 8 lanes of a quarter warp read 8
+//     neighbouring rays at one sample step, i.e. 8 texels along a digital
+//     line.  The bank slots of those addresses are simulated for both
+//     orientations (a transposed copy of the packed image serves "mostly
+//     vertical" lane lines), every row-pitch residue mod 8 and three per-lane
+//     tap orders, and the cheapest is kept;
+//   * the chunks: greedily, the longest t-interval (up to 48 units) whose box
+//     fits the shared-memory budget, so every CTA gets as few chunks (barriers)
+//     and as much texel reuse as its geometry allows.  Boxes come from the
+//     exact fp64 ray segments with one unit of slack in t and one texel around
+//     the taps (the kernel assigns samples to chunks in fp32).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -37,21 +44,20 @@ struct Pt {
 
 inline Pt to_pixel(double x, double y, double half) { return {x + half + 0.5, half - y + 0.5}; }
 
-// Bank-conflict cost of one orientation / pitch: sum over quarter warps and
-// taps of the number of distinct 16-byte cells that share a slot (1 = free).
+// Bank-conflict cost of one layout: sum over quarter warps and taps of the
+// number of distinct 16-byte cells that share a slot (1 = conflict free).
 // swap: 0 none, 1 odd lanes load the bottom row first, 2 odd lanes load the
-// right column first (kernel: which tap each lane issues in each of its four
-// 128-bit loads; spreads the quarter warp over more bank slots).
-double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, bool transposed, int pitch, int swap) {
+// right column first (the kernel issues each lane's four taps in that order).
+double conflict_cost(const std::vector<Pt>& lanes_at_step, bool transposed, int pitch, int swap) {
   double cost = 0.0;
-  const int nw = int(lanes_at_step.size()) / lanes_per_warp;
+  const int nw = int(lanes_at_step.size()) / 32;
   for (int w = 0; w < nw; ++w) {
-    for (int q = 0; q < lanes_per_warp; q += 8) {
+    for (int q = 0; q < 32; q += 8) {
       int64_t bi[8], bj[8];
       int lane_of[8];
       int used = 0;
-      for (int l = 0; l < 8 && q + l < lanes_per_warp; ++l) {
-        const Pt& pt = lanes_at_step[size_t(w * lanes_per_warp + q + l)];
+      for (int l = 0; l < 8; ++l) {
+        const Pt& pt = lanes_at_step[size_t(w * 32 + q + l)];
         if (std::isnan(pt.px)) continue;
         const double cx = transposed ? pt.py : pt.px, cy = transposed ? pt.px : pt.py;
         bj[used] = int64_t(std::floor(cx));
@@ -78,6 +84,13 @@ double conflict_cost(const std::vector<Pt>& lanes_at_step, int lanes_per_warp, b
   }
   return cost;
 }
+
+struct Box {
+  int64_t r0, c0, rows, cols;  // normal (untransposed) padded-image coordinates
+  bool empty() const { return rows <= 0; }
+};
+
+inline int pitch_for(int64_t cols, int residue) { return int(cols + ((residue - cols) % 8 + 8) % 8); }
 
 }  // namespace
 
@@ -110,12 +123,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     ray_aux[r] = make_float4(float(R.h), nf, float(R.t0), float(1.0 / R.h));
   }
 
-  // ---- CTA angle sets: angles sorted by direction (mod 2 pi: theta and theta + pi
-  // march the same lines in opposite t), A_eff consecutive ones per CTA (the
-  // reference accepts arbitrary angle lists, geometry.cpp:12-18)
   ForwardSchedule& F = p.fwd;
-  F.A = 8;
-  F.W = 32;
   std::vector<int> order(static_cast<size_t>(na));
   for (int64_t a = 0; a < na; ++a) order[size_t(a)] = int(a);
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
@@ -126,143 +134,197 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   const double R = half * std::sqrt(2.0);  // every image point lies within R of the centre
   const double t_lo = (fan ? p.g.source_distance : 0.0) - R - 1.0;
   const double t_hi = (fan ? p.g.source_distance : 0.0) + R + 1.0;
-  F.ctas_k = int((nd + F.W - 1) / F.W);
-  const int64_t box_budget = 6 * 1024;  // float4 cells (96 KB)
+  const int64_t nkb = (nd + 31) / 32;  // 32-cell detector blocks
+  int64_t budget = F.box_budget;
 
-  for (int a_eff : {8, 4, 2, 1}) {
-  F.ctas_a = int((na + a_eff - 1) / a_eff);
-  const int ctas = F.ctas_a * F.ctas_k;
-  F.slots.assign(size_t(F.ctas_a) * F.A, -1);
-  for (int64_t i = 0; i < na; ++i) F.slots[size_t((i / a_eff) * F.A + (i % a_eff))] = order[size_t(i)];
-  for (double tlen : {32.0, 24.0, 16.0, 12.0, 8.0, 6.0, 4.0}) {
-    F.tlen = float(tlen);
-    F.tbase = float(t_lo);
-    F.chunks = int(std::ceil((t_hi - t_lo) / tlen));
-    F.boxes.assign(size_t(ctas) * F.chunks, make_int4(0, 0, 0, 0));
-    F.cta.assign(size_t(ctas), make_int2(0, 0));
-    F.max_box = 0;
-    F.any_transposed = false;
-    auto plan_rows = [&](int ca_lo, int ca_hi, int64_t& max_box_out) {
-    std::vector<Pt> sim;
-    for (int ca = ca_lo; ca < ca_hi; ++ca) {
-      for (int ck = 0; ck < F.ctas_k; ++ck) {
-        const int cta = ca * F.ctas_k + ck;
-        int64_t maxcols[2] = {0, 0};
-        std::vector<int4> bx(size_t(F.chunks));  // normal orientation {row0, col0, rows, cols}
-        for (int c = 0; c < F.chunks; ++c) {
-          const double ta = double(F.tbase) + double(c) * tlen - 1.0;
-          const double tb = double(F.tbase) + double(c + 1) * tlen + 1.0;
-          double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
-          for (int ai = 0; ai < F.A; ++ai) {
-            const int a = F.slots[size_t(ca) * F.A + ai];
-            if (a < 0) continue;
-            for (int ki = 0; ki < F.W; ++ki) {
-              const int64_t k = int64_t(ck) * F.W + ki;
-              if (k >= nd) break;
-              const RayD& ry = rays[size_t(a * nd + k)];
-              if (ry.n == 0) continue;
-              const double u0 = std::max(ta, ry.t0), u1 = std::min(tb, ry.t1);
-              if (!(u1 >= u0)) continue;
-              for (double t : {u0, u1}) {
-                Pt q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
-                xmin = std::min(xmin, q.px);
-                xmax = std::max(xmax, q.px);
-                ymin = std::min(ymin, q.py);
-                ymax = std::max(ymax, q.py);
-              }
-            }
-          }
-          if (xmin > xmax) continue;  // no samples of this CTA in the chunk
-          int64_t c0 = std::max<int64_t>(0, int64_t(std::floor(xmin)) - 1);
-          int64_t c1 = std::min<int64_t>(P2 - 1, int64_t(std::floor(xmax)) + 2);
-          int64_t r0 = std::max<int64_t>(0, int64_t(std::floor(ymin)) - 1);
-          int64_t r1 = std::min<int64_t>(P2 - 1, int64_t(std::floor(ymax)) + 2);
-          bx[size_t(c)] = make_int4(int(r0), int(c0), int(r1 - r0 + 1), int(c1 - c0 + 1));
-          maxcols[0] = std::max(maxcols[0], c1 - c0 + 1);
-          maxcols[1] = std::max(maxcols[1], r1 - r0 + 1);
+  struct Shape {
+    int aa, db;
+  };
+
+  // Box of the samples of `warps` (8 x {angle, first cell}) with t in [ta, tb] (+1 slack).
+  auto box_of = [&](const int2* wa, double ta, double tb) {
+    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+    for (int w = 0; w < 8; ++w) {
+      if (wa[w].x < 0) continue;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t kk = int64_t(wa[w].y) + l;
+        if (kk >= nd) break;
+        const RayD& ry = rays[size_t(int64_t(wa[w].x) * nd + kk)];
+        if (ry.n == 0) continue;
+        const double u0 = std::max(ta - 1.0, ry.t0), u1 = std::min(tb + 1.0, ry.t1);
+        if (!(u1 >= u0)) continue;
+        for (double t : {u0, u1}) {
+          Pt q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
+          xmin = std::min(xmin, q.px);
+          xmax = std::max(xmax, q.px);
+          ymin = std::min(ymin, q.py);
+          ymax = std::max(ymax, q.py);
         }
-        // ---- orientation + pitch by simulated bank conflicts at a few aligned sample steps
+      }
+    }
+    Box b{0, 0, 0, 0};
+    if (xmin > xmax) return b;
+    const int64_t c0 = std::max<int64_t>(0, int64_t(std::floor(xmin)) - 1);
+    const int64_t c1 = std::min<int64_t>(P2 - 1, int64_t(std::floor(xmax)) + 2);
+    const int64_t r0 = std::max<int64_t>(0, int64_t(std::floor(ymin)) - 1);
+    const int64_t r1 = std::min<int64_t>(P2 - 1, int64_t(std::floor(ymax)) + 2);
+    return Box{r0, c0, r1 - r0 + 1, c1 - c0 + 1};
+  };
+
+  // Greedy chunking of one CTA for a layout: returns false if even the
+  // shortest chunk overflows the budget.  Appends {r0|c0<<16, rows|cols<<16, pitch, t_end bits}.
+  auto chunk_cta = [&](const int2* wa, bool tr, int residue, std::vector<int4>* out, int64_t* staged,
+                       int64_t* max_cells) -> bool {
+    double t = t_lo;
+    while (t < t_hi) {
+      bool placed = false;
+      for (double len : {48.0, 40.0, 32.0, 24.0, 16.0, 12.0, 8.0, 6.0, 4.0, 3.0, 2.0}) {
+        const double tb = std::min(t + len, t_hi);
+        Box b = box_of(wa, t, tb);
+        if (b.empty()) {
+          // nothing of this CTA here: skip ahead without a box
+          t = tb;
+          placed = true;
+          break;
+        }
+        const int64_t rows = tr ? b.cols : b.rows, cols = tr ? b.rows : b.cols;
+        const int pitch = pitch_for(cols, residue);
+        if (rows * pitch > budget && len > 2.0) continue;
+        if (rows * pitch > budget) return false;
+        if (out) {
+          const int64_t r0 = tr ? b.c0 : b.r0, c0 = tr ? b.r0 : b.c0;
+          float tend = tb >= t_hi ? INFINITY : float(tb);
+          int tbits;
+          std::memcpy(&tbits, &tend, 4);
+          out->push_back(make_int4(int(r0 | (c0 << 16)), int(rows | (cols << 16)), pitch, tbits));
+        }
+        if (staged) *staged += rows * cols;
+        if (max_cells) *max_cells = std::max(*max_cells, rows * pitch);
+        t = tb;
+        placed = true;
+        break;
+      }
+      if (!placed) return false;
+    }
+    return true;
+  };
+
+  auto warps_of = [&](Shape sh) {
+    const int ctas_a = int((na + sh.aa - 1) / sh.aa);
+    const int ctas_k = int((nkb + sh.db - 1) / sh.db);
+    std::vector<int2> warps(size_t(ctas_a) * ctas_k * 8, make_int2(-1, 0));
+    for (int ca = 0; ca < ctas_a; ++ca)
+      for (int ck = 0; ck < ctas_k; ++ck)
+        for (int w = 0; w < sh.aa * sh.db; ++w) {
+          const int64_t ai = int64_t(ca) * sh.aa + w / sh.db;
+          const int64_t kb = int64_t(ck) * sh.db + w % sh.db;
+          if (ai < na && kb < nkb) warps[size_t(ca * ctas_k + ck) * 8 + w] = make_int2(order[size_t(ai)], int(kb * 32));
+        }
+    return warps;
+  };
+
+  // Per-CTA layout by simulation, then greedy chunks (parallel over CTAs).
+  struct CtaPlan {
+    int tr = 0, residue = 0, swap = 0;
+    bool ok = false;
+    int64_t staged = 0, max_cells = 0;
+    std::vector<int4> boxes;
+  };
+  auto plan_shape = [&](Shape sh, std::vector<CtaPlan>& plans) {
+    std::vector<int2> warps = warps_of(sh);
+    const int ctas = int(warps.size() / 8);
+    plans.assign(size_t(ctas), CtaPlan{});
+    auto work = [&](int lo, int hi) {
+      std::vector<Pt> sim;
+      for (int cta = lo; cta < hi; ++cta) {
+        const int2* wa = &warps[size_t(cta) * 8];
+        CtaPlan& cp = plans[size_t(cta)];
+        // lane positions at a few aligned steps of the march
         sim.clear();
-        const int steps = 4;
-        for (int st = 0; st < steps; ++st) {
-          const double tt = t_lo + (t_hi - t_lo) * (0.2 + 0.6 * double(st) / double(steps - 1));
-          for (int ai = 0; ai < F.A; ++ai) {
-            const int a = F.slots[size_t(ca) * F.A + ai];
-            for (int ki = 0; ki < F.W; ++ki) {
-              const int64_t k = int64_t(ck) * F.W + ki;
+        for (int st = 0; st < 4; ++st) {
+          const double tt = t_lo + (t_hi - t_lo) * (0.2 + 0.6 * double(st) / 3.0);
+          for (int w = 0; w < 8; ++w)
+            for (int l = 0; l < 32; ++l) {
               Pt q{NAN, NAN};
-              if (a >= 0 && k < nd) {
-                const RayD& ry = rays[size_t(a * nd + k)];
+              const int64_t kk = int64_t(wa[w].y) + l;
+              if (wa[w].x >= 0 && kk < nd) {
+                const RayD& ry = rays[size_t(int64_t(wa[w].x) * nd + kk)];
                 if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
-                  // the sample the lane reaches when the chunk-aligned march is at tt
-                  double m = std::floor((tt - ry.t0) / ry.h);
-                  double t = ry.t0 + (m + 0.5) * ry.h;
+                  const double m = std::floor((tt - ry.t0) / ry.h);
+                  const double t = ry.t0 + (m + 0.5) * ry.h;
                   q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
                 }
               }
               sim.push_back(q);
             }
-          }
         }
         double best = 1e300;
-        int best_pitch = int(maxcols[0]), best_tr = 0, best_swap = 0;
-        for (int tr = 0; tr < 2; ++tr) {
-          if (maxcols[tr] == 0) continue;
-          for (int swap = 0; swap < 3; ++swap) {
-            for (int d = 0; d < 8; ++d) {
-              const int pitch = int(maxcols[tr]) + d;
-              const double cst =
-                  conflict_cost(sim, F.W, tr == 1, pitch, swap) * (1.0 + 1e-4 * d + 1e-3 * tr + 1e-5 * swap);
-              if (cst < best) {
-                best = cst;
-                best_pitch = pitch;
-                best_tr = tr;
-                best_swap = swap;
-              }
+        for (int tr = 0; tr < 2; ++tr)
+          for (int swap = 0; swap < 3; ++swap)
+            for (int res = 0; res < 8; ++res) {
+              const double c = conflict_cost(sim, tr == 1, 64 + res, swap) * (1.0 + 1e-3 * tr + 1e-5 * swap);
+              if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap;
             }
-          }
-        }
-        // cfg.y: bit 0 transposed image, bits 1-2 per-lane tap order
-        F.cta[size_t(cta)] = make_int2(best_pitch, best_tr | (best_swap << 1));
-        for (int c = 0; c < F.chunks; ++c) {
-          int4 b = bx[size_t(c)];
-          if (b.z == 0) continue;
-          if (best_tr) b = make_int4(b.y, b.x, b.w, b.z);  // box in transposed-image coordinates
-          F.boxes[size_t(cta) * F.chunks + c] = b;
-          max_box_out = std::max<int64_t>(max_box_out, int64_t(b.z) * best_pitch);
-        }
+        cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
       }
-    }
     };
-    const int nthreads = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), F.ctas_a));
-    std::vector<int64_t> mb(size_t(nthreads), 0);
+    const int nthreads = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), ctas));
     std::vector<std::thread> pool;
-    for (int t = 0; t < nthreads; ++t) {
-      const int lo = int(int64_t(F.ctas_a) * t / nthreads), hi = int(int64_t(F.ctas_a) * (t + 1) / nthreads);
-      pool.emplace_back(plan_rows, lo, hi, std::ref(mb[size_t(t)]));
-    }
+    for (int t = 0; t < nthreads; ++t)
+      pool.emplace_back(work, int(int64_t(ctas) * t / nthreads), int(int64_t(ctas) * (t + 1) / nthreads));
     for (auto& th : pool) th.join();
-    for (int64_t v : mb) F.max_box = std::max(F.max_box, v);
-    for (const int2& c : F.cta) F.any_transposed |= (c.y & 1) == 1;
-    if (F.max_box <= box_budget) {
-      if (std::getenv("RK_DEBUG_PLAN")) {
-        int64_t boxes = 0, cells = 0, ntr = 0;
-        for (const int4& b : F.boxes)
-          if (b.z) ++boxes, cells += int64_t(b.z) * b.w;
-        for (const int2& c : F.cta) ntr += c.y & 1;
-        std::fprintf(stderr,
-                     "[rk] forward schedule: %d angles/CTA, tlen %.0f, %d chunks, %d CTAs (%lld transposed), "
-                     "%lld boxes, mean box %.0f texels, max box %lld cells (%.1f KB), staged texels per image "
-                     "%.2fM\n",
-                     a_eff, double(F.tlen), F.chunks, ctas, (long long)ntr, (long long)boxes,
-                     boxes ? double(cells) / double(boxes) : 0.0, (long long)F.max_box,
-                     double(F.max_box) * 16.0 / 1024.0, double(cells) / 1e6);
-      }
-      return;
+    return warps;
+  };
+
+  // 8 angles x 32 cells is the reuse-friendly shape (adjacent angles of a sorted
+  // list march nearly parallel rays).  Fallbacks, in order, when some CTA
+  // cannot fit even its shortest chunk (sparse or scattered angle lists):
+  // wider detector blocks, then a 192 KB budget (one CTA per SM), then CTAs
+  // with idle warps (fewer rays, smaller boxes).
+  struct Tier {
+    Shape sh;
+    int64_t budget;
+  };
+  const Tier tiers[] = {{{8, 1}, 4096},  {{4, 2}, 4096},  {{2, 4}, 4096},  {{1, 8}, 4096},  {{8, 1}, 12288},
+                        {{4, 2}, 12288}, {{4, 1}, 12288}, {{2, 1}, 12288}, {{1, 1}, 12288}};
+  for (const Tier& tier : tiers) {
+    const Shape sh = tier.sh;
+    if (sh.db > 1 && nkb < sh.db && sh.db != 8) continue;
+    budget = tier.budget;
+    std::vector<CtaPlan> plans;
+    std::vector<int2> warps = plan_shape(sh, plans);
+    bool ok = true;
+    for (const CtaPlan& cp : plans) ok &= cp.ok;
+    if (!ok) continue;
+    F.shape_aa = sh.aa;
+    F.shape_db = sh.db;
+    F.warps = std::move(warps);
+    F.cta.assign(plans.size(), make_int4(0, 0, 0, 0));
+    F.boxes.clear();
+    F.max_box = 0;
+    F.staged_texels = 0;
+    F.any_transposed = false;
+    for (size_t c = 0; c < plans.size(); ++c) {
+      const CtaPlan& cp = plans[c];
+      F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()), cp.tr | (cp.swap << 1), 0);
+      F.boxes.insert(F.boxes.end(), cp.boxes.begin(), cp.boxes.end());
+      F.max_box = std::max(F.max_box, cp.max_cells);
+      F.staged_texels += cp.staged;
+      F.any_transposed |= cp.tr == 1;
     }
+    if (std::getenv("RK_DEBUG_PLAN")) {
+      int64_t ntr = 0;
+      for (const int4& c : F.cta) ntr += c.z & 1;
+      std::fprintf(stderr,
+                   "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
+                   "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
+                   sh.aa, sh.db, F.cta.size(), (long long)ntr, F.boxes.size(),
+                   double(F.boxes.size()) / double(F.cta.size()), (long long)F.max_box,
+                   double(F.max_box) * 16.0 / 1024.0, double(F.staged_texels) / 1e6);
+    }
+    return;
   }
-  }
-  throw ValidationError("forward schedule: no chunk length keeps the staged image box within shared memory");
+  throw ValidationError("forward schedule: a staged image box exceeds shared memory even for the shortest chunk");
 }
 
 }  // namespace rk

@@ -129,30 +129,26 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 template <class TOut>
 __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
-    const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int2* __restrict__ cta_cfg,
-    const int* __restrict__ slots, int na, int nd, int chunks, float tbase, float tlen, int ctas_k, int64_t batch,
-    TOut* __restrict__ sino, FwdEpilogue epi) {
+    const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
+    const int2* __restrict__ warps, int na, int nd, int64_t batch, TOut* __restrict__ sino, FwdEpilogue epi) {
   extern __shared__ float4 box_s[];
   const int cta = blockIdx.x;
-  const int ga = cta / ctas_k, gk = cta - ga * ctas_k;
   const int64_t g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a = __ldg(slots + ga * (kFwdThreads / 32) + warp), k = gk * 32 + lane;  // angles sorted by direction
+  const int2 wa = __ldg(warps + cta * (kFwdThreads / 32) + warp);  // {angle, first cell}; angles sorted by direction
+  const int a = wa.x, k = wa.y + lane;
   const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
-  const int2 cfg = cta_cfg[cta];
-  const int pitch = cfg.x;
-  const bool tr = (cfg.y & 1) != 0;
+  const int4 cfg = __ldg(cta_cfg + cta);  // {first box, boxes, flags}
+  const bool tr = (cfg.z & 1) != 0;
   // Per-lane tap order chosen by the planner against bank conflicts: odd lanes
   // issue the bottom row first (swap 1) or the right column first (swap 2).
   // Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA) (rowB,colB); the
   // weights follow the same order, so no value is moved between registers.
-  const int swap = (cfg.y >> 1) & 3;
+  const int swap = (cfg.z >> 1) & 3;
   const bool odd = (threadIdx.x & 1) != 0;
   const bool rs = swap == 1 && odd, cs = swap == 2 && odd;
-  const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
   const int dX = cs ? -1 : 1;
-  const int dY = rs ? -pitch : pitch;
   float4 G = make_float4(0.f, 0.f, 0.f, 0.f), X = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     G = __ldg(ray_geom + r);
@@ -164,28 +160,29 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
   const float t0 = X.z, inv_h = X.w;
   const int P = s + 2;
   const float4* src = (tr ? img_t : img) + g * int64_t(P) * P;
-  const int4* bxs = boxes + int64_t(cta) * chunks;
+  const int4* bxs = boxes + cfg.x;
 
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   int m = 0;
-  for (int c = 0; c < chunks; ++c) {
+  for (int c = 0; c < cfg.y; ++c) {
     const int4 bx = __ldg(bxs + c);  // CTA-uniform
-    if (bx.z == 0) continue;
-    int m_end = n;
-    if (c + 1 < chunks) {
-      const float tn = fmaf(float(c + 1), tlen, tbase);
-      m_end = min(max(int(ceilf(fmaf(tn - t0, inv_h, -0.5f))), 0), n);
-    }
+    const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16, pitch = bx.z;
+    const float tend = __int_as_float(bx.w);
+    // samples of this chunk: t_m < t_end  <=>  m < ceil((t_end - t0) / h - 0.5)
+    const int m_end =
+        isinf(tend) ? n : min(max(int(ceilf(fmaf(tend - t0, inv_h, -0.5f))), 0), n);
     __syncthreads();  // previous chunk's samples are done with the box
-    for (int rr = warp; rr < bx.z; rr += kFwdThreads / 32) {
-      const float4* srow = src + int64_t(bx.x + rr) * P + bx.y;
+    for (int rr = warp; rr < rows; rr += kFwdThreads / 32) {
+      const float4* srow = src + int64_t(r0 + rr) * P + c0;
       float4* drow = box_s + rr * pitch;
-      for (int cc = lane; cc < bx.w; cc += 32) cp_async16(drow + cc, srow + cc);
+      for (int cc = lane; cc < cols; cc += 32) cp_async16(drow + cc, srow + cc);
     }
     cp_async_wait_all();
     __syncthreads();
-    const float ox = float(bx.y), oy = float(bx.x);
-    const int jmax = bx.w - 2, imax = bx.z - 2;
+    const float ox = float(c0), oy = float(r0);
+    const int jmax = cols - 2, imax = rows - 2;
+    const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
+    const int dY = rs ? -pitch : pitch;
     for (; m < m_end; ++m) {
       const float t = float(m) + 0.5f;
       const float px = fmaf(t, hx, px0) - ox;  // exact shift: the box origin is an integer
@@ -238,13 +235,31 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
 // Per-angle constants of one tile.  Parallel beam: kf - ws is affine in the
 // pixel offsets, fp32 suffices (no magnification).  Fan beam: the pixel ->
 // detector map u = qx * span / (qy + D_so) magnifies position errors by
-// span / (qy + D_so) (large near the source), so the per-pixel geometry runs
-// in fp64 (B200's fp64 rate keeps it off the critical path).
+// span / (sp (qy + D_so)).  kBpFan32 evaluates it relative to the tile corner,
+//   kf - ws = base + (dq K - u00 dd) / (den00 + dd),   dq, dd = O(tile) offsets,
+// which keeps fp32 accurate for moderate magnification; kBpFan64 (source close
+// to the image, plan.cpp picks it) runs the per-pixel map in fp64.
+enum { kBpParallel = 0, kBpFan32 = 1, kBpFan64 = 2 };
 struct ParConst {
   float base, cx, cy, pad;
 };
+struct Fan32Const {
+  float base, u00, den00, c, s, pad0, pad1, pad2;
+};
 struct FanConst {
   double qx00, den00, c, s, offw, pad;
+};
+template <int KIND>
+struct BpConst {
+  using type = ParConst;
+};
+template <>
+struct BpConst<kBpFan32> {
+  using type = Fan32Const;
+};
+template <>
+struct BpConst<kBpFan64> {
+  using type = FanConst;
 };
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -257,12 +272,12 @@ constexpr int kTile = 32;
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 
-template <bool FAN, class TOut>
-__global__ void __launch_bounds__(kBpThreads) backproject_kernel(
+template <int KIND, class TOut>
+__global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, int window, int chunk, int64_t batch,
     TOut* __restrict__ out, BpEpilogue epi) {
-  using Const = typename std::conditional<FAN, FanConst, ParConst>::type;
+  using Const = typename BpConst<KIND>::type;
   extern __shared__ float4 smem[];
   float4* win = smem;                                                    // chunk * window cells
   Const* cst = reinterpret_cast<Const*>(smem + size_t(chunk) * window);  // chunk records
@@ -294,7 +309,7 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
       const double x1 = x0 + double(min(kTile, s - j0) - 1), y1 = y0 - double(min(kTile, s - i0) - 1);
       double lo;
       Const k;
-      if constexpr (!FAN) {
+      if constexpr (KIND == kBpParallel) {
         const double k00 = (x0 * c + y0 * sn) / spacing + off;
         const double k10 = (x1 * c + y0 * sn) / spacing + off;
         const double k01 = (x0 * c + y1 * sn) / spacing + off;
@@ -311,14 +326,26 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
           const double qx = x * c + y * sn, qy = -x * sn + y * c;
           return (qx * span / (qy + source_distance)) / spacing + off;
         };
-        lo = fmin(fmin(kfan(x0, y0), kfan(x1, y0)), fmin(kfan(x0, y1), kfan(x1, y1)));
+        const double k00 = kfan(x0, y0);
+        lo = fmin(fmin(k00, kfan(x1, y0)), fmin(kfan(x0, y1), kfan(x1, y1)));
         const int ws = max(int(floor(lo)) - 1, -2);  // clipped like the host window (plan.cpp)
-        k.qx00 = x0 * c + y0 * sn;
-        k.den00 = -x0 * sn + y0 * c + source_distance;
-        k.c = c;
-        k.s = sn;
-        k.offw = off - double(ws);
-        k.pad = 0.0;
+        const double qx00 = x0 * c + y0 * sn;
+        const double den00 = -x0 * sn + y0 * c + source_distance;
+        if constexpr (KIND == kBpFan32) {
+          k.base = float(k00 - double(ws));
+          k.u00 = float(qx00 * (span / spacing) / den00);
+          k.den00 = float(den00);
+          k.c = float(c);
+          k.s = float(sn);
+          k.pad0 = k.pad1 = k.pad2 = 0.f;
+        } else {
+          k.qx00 = qx00;
+          k.den00 = den00;
+          k.c = c;
+          k.s = sn;
+          k.offw = off - double(ws);
+          k.pad = 0.0;
+        }
         ws_s[tid] = ws;
       }
       cst[tid] = k;
@@ -335,6 +362,7 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
     __syncthreads();
     // ---- accumulate
     const double kmag = span / spacing;
+    const float kmag_f = float(kmag);
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
       const float4* w = win + q * window;
@@ -342,8 +370,13 @@ __global__ void __launch_bounds__(kBpThreads) backproject_kernel(
       for (int r = 0; r < kRowsPerThread; ++r) {
         const float lx = float(tx), ly = float(ty + r * (kTile / kRowsPerThread));
         float kf;
-        if constexpr (!FAN) {
+        if constexpr (KIND == kBpParallel) {
           kf = fmaf(lx, k.cx, fmaf(ly, k.cy, k.base));
+        } else if constexpr (KIND == kBpFan32) {
+          const float dq = fmaf(lx, k.c, -ly * k.s);   // qx - qx00
+          const float dd = fmaf(-lx, k.s, -ly * k.c);  // den - den00
+          const float num = fmaf(dq, kmag_f, -k.u00 * dd);
+          kf = fmaf(num, rcp_approx(k.den00 + dd), k.base);
         } else {
           const double dlx = double(lx), dly = double(ly);
           const double qx = fma(dlx, k.c, fma(-dly, k.s, k.qx00));
@@ -436,7 +469,7 @@ void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4
 void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
   const ForwardSchedule& F = p.fwd;
-  dim3 grid(unsigned(F.ctas_a * F.ctas_k), unsigned(groups_of(batch)));
+  dim3 grid(unsigned(F.cta.size()), unsigned(groups_of(batch)));
   const size_t smem = size_t(F.max_box) * sizeof(float4);
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
@@ -444,8 +477,8 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FORWARD, st);
     kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
-                                         p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int2>(),
-                                         p.fwd_slots.as<int>(), int(p.na), int(p.nd), F.chunks, F.tbase, F.tlen, F.ctas_k, batch,
+                                         p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int4>(),
+                                         p.fwd_warps.as<int2>(), int(p.na), int(p.nd), batch,
                                          static_cast<T*>(sino), epi);
   });
   RK_CUDA(cudaGetLastError());
@@ -456,12 +489,13 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
   const int tiles = int((p.s + kTile - 1) / kTile);
   dim3 grid(tiles, tiles, unsigned(groups_of(batch)));
   dim3 block(kTile, kTile / kRowsPerThread);
-  const bool fan = p.g.kind == RK_FANBEAM;
-  const size_t smem = size_t(p.bp_angle_chunk) * p.bp_window * sizeof(float4) +
-                      size_t(p.bp_angle_chunk) * ((fan ? sizeof(FanConst) : sizeof(ParConst)) + sizeof(int));
+  const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
+  const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
+  const size_t smem = size_t(p.bp_angle_chunk) * p.bp_window * sizeof(float4) + size_t(p.bp_angle_chunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = fan ? backproject_kernel<true, T> : backproject_kernel<false, T>;
+    auto kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T>
+                                    : kind == kBpFan32 ? backproject_kernel<kBpFan32, T> : backproject_kernel<kBpFan64, T>;
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,

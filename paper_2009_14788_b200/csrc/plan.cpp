@@ -209,6 +209,13 @@ void build_plan(Plan& p) {
     throw ValidationError("backprojection window of " + std::to_string(window) +
                           " detector cells exceeds shared memory (det_count too large)");
   p.bp_window = int(window);
+  // fp32 (tile-relative) fan map unless the magnification span / (sp (D_so - R))
+  // of the pixels nearest the source is large (kernels.cu, kBpFan32 / kBpFan64)
+  if (fan) {
+    const double rmax = half * std::sqrt(2.0);
+    const double mag = span / (g.det_spacing * (g.source_distance - rmax));
+    p.bp_fan_fp64 = !(mag <= 8.0);
+  }
   // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to 192 KB)
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(32, (32 * 1024) / (window * 16)));
   p.bp_angle_chunk = int(chunk);
@@ -222,11 +229,11 @@ void build_plan(Plan& p) {
   RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.ray_aux.ptr, ra.data(), ra.size() * sizeof(float4), cudaMemcpyHostToDevice));
   p.fwd_boxes.reserve(p.fwd.boxes.size() * sizeof(int4));
-  p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int2));
+  p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int4));
   RK_CUDA(cudaMemcpy(p.fwd_boxes.ptr, p.fwd.boxes.data(), p.fwd.boxes.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  p.fwd_slots.reserve(p.fwd.slots.size() * sizeof(int));
-  RK_CUDA(cudaMemcpy(p.fwd_slots.ptr, p.fwd.slots.data(), p.fwd.slots.size() * sizeof(int), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  p.fwd_warps.reserve(p.fwd.warps.size() * sizeof(int2));
+  RK_CUDA(cudaMemcpy(p.fwd_warps.ptr, p.fwd.warps.data(), p.fwd.warps.size() * sizeof(int2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaEventCreateWithFlags(&p.scratch_free, cudaEventDisableTiming));
 }

@@ -71,17 +71,16 @@ struct RayD {
 };
 
 struct ForwardSchedule {
-  int A = 8;        // angles per CTA (one warp each)
-  int W = 32;       // detectors per CTA (one lane each)
-  float tbase = 0;  // t of the first chunk boundary
-  float tlen = 0;   // chunk length along the ray (world units)
-  int chunks = 0;
-  int ctas_a = 0, ctas_k = 0;
-  int64_t max_box = 0;  // largest rows * pitch over all boxes (float4 cells)
+  int64_t box_budget = 4096;       // float4 cells per staged box (64 KB: three CTAs per SM)
+  int shape_aa = 8, shape_db = 1;  // angles x 32-cell detector blocks per CTA
+  int64_t max_box = 0;             // largest rows * pitch over all boxes (float4 cells)
+  int64_t staged_texels = 0;       // per image group, all CTAs and chunks
   bool any_transposed = false;
-  std::vector<int4> boxes;  // ctas * chunks
-  std::vector<int2> cta;    // ctas
-  std::vector<int> slots;   // ctas_a * A angle indices (-1: idle warp)
+  // per chunk {row0 | col0 << 16, rows | cols << 16, pitch, t_end (float bits; inf = last)},
+  // in staged-image coordinates, CTA after CTA
+  std::vector<int4> boxes;
+  std::vector<int4> cta;    // per CTA {first box, box count, bit0 transposed | bits1-2 lane tap order, 0}
+  std::vector<int2> warps;  // per CTA x 8 warps {angle (-1: idle), first detector cell}
 };
 
 // ----------------------------------------------------------------- plan
@@ -103,13 +102,14 @@ struct Plan {
   // are marched chunk by chunk along t, each chunk's image footprint (box) is
   // staged in shared memory
   ForwardSchedule fwd;
-  DeviceBuffer fwd_boxes;  // int4 {row0, col0, rows, cols} per (cta, chunk), staged-image coordinates
-  DeviceBuffer fwd_cta;    // int2 {pitch, transposed} per cta
-  DeviceBuffer fwd_slots;  // int angle index per (cta row, warp), -1 = idle
+  DeviceBuffer fwd_boxes;  // int4 per chunk (see ForwardSchedule::boxes)
+  DeviceBuffer fwd_cta;    // int4 per CTA
+  DeviceBuffer fwd_warps;  // int2 {angle, first detector} per (cta, warp); angle -1 = idle
   // backprojection: per-angle trig in fp64
   DeviceBuffer trig;       // double2 {cos, sin}
   int bp_window = 0;       // staged detector cells per (tile, angle)
   int bp_angle_chunk = 0;  // angles staged per pass
+  bool bp_fan_fp64 = false;  // fan beam with the source close to the image: fp64 pixel map
 
   // scratch (serialised by `mu`; `scratch_free` orders reuse across streams)
   std::mutex mu;
