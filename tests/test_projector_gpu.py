@@ -207,3 +207,61 @@ def test_half_accuracy_vs_single(rk, oracle, cuda):
     bs = host(rk.backprojection(g, dev(fs, cuda)))
     bh = host(rk.backprojection(g, dev(fs.astype(np.float16), cuda)))
     assert rel_l2(bh, bs) < 1e-3
+
+
+def _random_geometry(rk, rs, fan):
+    s = int(rs.choice([1, 2, 3, 5, 17, 40, 64, 97]))
+    na = int(rs.integers(1, 40))
+    nd = int(rs.integers(1, 3 * s + 8))
+    sp = float(rs.uniform(0.3, 2.5))
+    ang = list(rs.uniform(-7.0, 7.0, na))  # arbitrary, unsorted, beyond 2 pi (geometry.cpp:12-18)
+    if not fan:
+        return rk.make_parallel(s, ang, nd, sp)
+    src = float(s) * float(rs.uniform(0.75, 4.0))
+    return rk.make_fanbeam(s, ang, src, float(rs.uniform(0.5, 3.0)) * s, nd, sp)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_geometry_parity(rk, oracle, cuda, seed):
+    """Arbitrary angle lists, tiny and odd sizes, any detector count/spacing, fan distances, steps."""
+    rs = np.random.default_rng(100 + seed)
+    g = _random_geometry(rk, rs, fan=seed % 2 == 1)
+    step = float(rs.choice([1.0, 0.5, 1.7]))
+    B = int(rs.integers(1, 7))
+    x = rs.standard_normal((B, g.image_size, g.image_size)).astype(np.float32)
+    f = host(rk.forward(g, dev(x, cuda), rk.ProjectorOptions(step)))
+    rf = oracle.forward(ogeom(g, step), x)
+    if np.abs(rf).max() > 0:
+        assert rel_l2(f, rf) <= TOL32, (g, step)
+    else:
+        assert np.abs(f).max() == 0
+    y = rs.standard_normal((B, g.n_angles, g.det_count)).astype(np.float32)
+    b = host(rk.backprojection(g, dev(y, cuda)))
+    rb = oracle.backprojection(ogeom(g), y)
+    if np.abs(rb).max() > 0:
+        assert rel_l2(b, rb) <= TOL32, g
+    else:
+        assert np.abs(b).max() == 0
+
+
+def test_half_overflow_is_unchecked_inf(rk, oracle, cuda):
+    """Tensor::from_double_as narrows to half unchecked (tensor.cpp:121-122): overflow -> inf, like the reference."""
+    g = par(rk, 64, 512)
+    y = np.full((1, 512, 64), 200.0, np.float16)
+    b = host(rk.backprojection(g, dev(y, cuda)))
+    rb = oracle.backprojection(ogeom(g), y)
+    assert np.array_equal(np.isinf(b), np.isinf(rb)) and np.isinf(b).any()
+    fin = np.isfinite(rb)
+    assert rel_l2(b[fin], rb[fin]) <= TOL16
+
+
+def test_large_batch_shards_equal(rk, oracle, cuda):
+    """Config-2 geometry: results are independent of how the batch is split (GPU-count invariance)."""
+    g = par(rk, 512, 512)
+    x = dev(batched_phantom(oracle, 512, 10), cuda)
+    full = rk.forward(g, x)
+    parts = torch.cat([rk.forward(g, x[:3]), rk.forward(g, x[3:8]), rk.forward(g, x[8:])])
+    assert torch.equal(full, parts)
+    bf = rk.backprojection(g, full)
+    bp = torch.cat([rk.backprojection(g, full[:6]), rk.backprojection(g, full[6:])])
+    assert torch.equal(bf, bp)
