@@ -1,0 +1,302 @@
+"""Command-line front end for the hot path — the subcommands of the reference
+CLI that reach it (``proj/tools/cli.cpp``): ``project``, ``backproject``,
+``filter``, ``fbp``, ``solve``, ``check-adjoint`` and ``bench``, with the same
+flags (angles in degrees, geometry defaults, ``--precision``), ``.npy`` files
+holding the natural rank (a batch dim is lifted/squeezed like
+``lift_batch``/``squeeze_batch``, cli.cpp:109-129), the same ``--json``
+reports (bench schema cli.cpp:662-676) and exit codes (0 ok, 1 validation,
+2 numerical; cli.cpp:718-730).  Every computation runs on the GPU.
+
+    python -m paper_2009_14788_b200 [--json] bench --size 512 --batch 32
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+import time
+
+import numpy as np
+
+from .errors import NumericalError, ValidationError
+
+VERSION = "radon_b200 0.1"
+
+
+def _geo_args(p, admm_names=False):
+    p.add_argument("--geometry", default="parallel", choices=["parallel", "fanbeam"])
+    p.add_argument("--angles", type=int, default=0, help="projection angle count (default: from input / size)")
+    p.add_argument("--angle-start", type=float, default=math.nan, help="first angle in degrees (default 0)")
+    p.add_argument("--angle-range", type=float, default=math.nan, help="span in degrees (180 parallel, 360 fan)")
+    p.add_argument("--det-count", type=int, default=0)
+    p.add_argument("--det-spacing", type=float, default=0.0)
+    p.add_argument("--source-distance", type=float, default=0.0, help="fan-beam (default: image size)")
+    p.add_argument("--det-distance", type=float, default=0.0, help="fan-beam (default: source distance)")
+    p.add_argument("--step", type=float, default=1.0)
+
+
+def build_geometry(a, image_size, n_angles):
+    """cli.cpp:76-97 (degrees -> radians through angles_linspace)."""
+    import paper_2009_14788_b200 as rk
+
+    if n_angles < 1:
+        raise ValidationError(f"angle count must be >= 1, got {n_angles}")
+    rng = a.angle_range if not math.isnan(a.angle_range) else (360.0 if a.geometry == "fanbeam" else 180.0)
+    start = a.angle_start if not math.isnan(a.angle_start) else 0.0
+    ang = [d * (math.pi / 180.0) for d in rk.angles_linspace(start, start + rng, n_angles)]
+    dc = a.det_count if a.det_count > 0 else None
+    ds = a.det_spacing if a.det_spacing > 0 else None
+    if a.geometry == "fanbeam":
+        src = a.source_distance if a.source_distance > 0 else float(image_size)
+        dd = a.det_distance if a.det_distance > 0 else None
+        return rk.make_fanbeam(image_size, ang, src, dd, dc, ds)
+    return rk.make_parallel(image_size, ang, dc, ds)
+
+
+def geometry_json(g):
+    """cli.cpp:140-159."""
+    if hasattr(g, "source_distance"):
+        return {"kind": "fanbeam", "image_size": g.image_size, "n_angles": g.n_angles,
+                "source_distance": g.source_distance, "det_distance": g.det_distance, "det_count": g.det_count,
+                "det_spacing": g.det_spacing}
+    return {"kind": "parallel", "image_size": g.image_size, "n_angles": g.n_angles, "det_count": g.det_count,
+            "det_spacing": g.det_spacing}
+
+
+_PREC = {"half": np.float16, "single": np.float32, "double": np.float64}
+
+
+def _read(path, want):
+    x = np.load(path)
+    if x.ndim == want - 1:
+        x = x[None]
+    elif x.ndim != want:
+        raise ValidationError(f"expected a {want - 1}-d or batched {want}-d array, got shape {x.shape}")
+    if x.dtype not in (np.float16, np.float32, np.float64):
+        raise ValidationError(f"unsupported dtype {x.dtype}")
+    return x
+
+
+def _apply_precision(x, name):
+    if not name:
+        return x
+    dt = _PREC[name]
+    if dt == np.float16 and x.dtype != np.float16:
+        f = x.astype(np.float32)
+        h = f.astype(np.float16)
+        bad = np.isinf(h) & np.isfinite(f)
+        if bad.any():  # to_half_storage is checked (tensor.cpp:241-265)
+            from .errors import HalfOverflowError
+
+            i = int(np.flatnonzero(bad)[0])
+            raise HalfOverflowError(f"value {float(f.flat[i])} at flat index {i} overflows half precision", i)
+        return h
+    return x.astype(dt)
+
+
+def _write(path, x):
+    np.save(path, x[0] if x.ndim >= 2 and x.shape[0] == 1 else x)
+
+
+def _to_dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _host(t):
+    return t.detach().cpu().numpy()
+
+
+def main(argv=None) -> int:
+    import paper_2009_14788_b200 as rk
+
+    ap = argparse.ArgumentParser(prog="python -m paper_2009_14788_b200", description=__doc__.split("\n")[0])
+    ap.add_argument("--json", action="store_true", help="emit reports as JSON on stdout")
+    ap.add_argument("--version", action="version", version=VERSION)
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    p = sub.add_parser("project", help="forward-project an image to a sinogram")
+    _geo_args(p)
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--precision", choices=list(_PREC), default="")
+    p = sub.add_parser("backproject", help="backproject a sinogram to an image")
+    _geo_args(p)
+    p.add_argument("--size", type=int, required=True)
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--precision", choices=list(_PREC), default="")
+    p = sub.add_parser("filter", help="apply a reconstruction filter to a sinogram")
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--filter", default="ram-lak", choices=["ram-lak", "shepp-logan", "cosine", "hamming", "hann"])
+    p = sub.add_parser("fbp", help="filtered backprojection reconstruction")
+    _geo_args(p)
+    p.add_argument("--size", type=int, required=True)
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--filter", default="ram-lak", choices=["ram-lak", "shepp-logan", "cosine", "hamming", "hann"])
+    p.add_argument("--reference", default="")
+    p.add_argument("--precision", choices=list(_PREC), default="")
+    p = sub.add_parser("solve", help="iterative reconstruction from a sinogram")
+    _geo_args(p)
+    p.add_argument("--method", required=True, choices=["landweber", "cg", "cgne"])
+    p.add_argument("--iterations", type=int, default=100)
+    p.add_argument("--alpha", type=float, default=0.0)
+    p.add_argument("--alpha-iterations", type=int, default=20)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--tolerance", type=float, default=0.0)
+    p.add_argument("--size", type=int, required=True)
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--reference", default="")
+    p.add_argument("--precision", choices=list(_PREC), default="")
+    p = sub.add_parser("check-adjoint", help="dot-product test of the projector pair")
+    _geo_args(p)
+    p.add_argument("--size", type=int, default=64)
+    p.add_argument("--trials", type=int, default=8)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--tolerance", type=float, default=0.0)
+    p = sub.add_parser("bench", help="time forward and backprojection throughput")
+    _geo_args(p)
+    p.add_argument("--size", type=int, default=512)
+    p.add_argument("--batch", type=int, default=1)
+    p.add_argument("--precision", choices=list(_PREC), default="single")
+    p.add_argument("--warmup", type=int, default=1)
+    p.add_argument("--runs", type=int, default=5)
+    a = ap.parse_args(argv)
+    try:
+        return _run(rk, a)
+    except ValidationError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except NumericalError as e:
+        print(f"numerical error: {e}", file=sys.stderr)
+        return 2
+
+
+def _run(rk, a) -> int:
+    import torch
+
+    if a.cmd == "project":  # cli.cpp:261-273
+        img = _apply_precision(_read(a.inp, 3), a.precision)
+        g = build_geometry(a, img.shape[1], a.angles if a.angles > 0 else img.shape[1])
+        _write(a.out, _host(rk.forward(g, _to_dev(img), rk.ProjectorOptions(a.step))))
+        return 0
+    if a.cmd == "backproject":  # cli.cpp:283-299
+        sino = _apply_precision(_read(a.inp, 3), a.precision)
+        if a.det_count == 0:
+            a.det_count = sino.shape[2]
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else sino.shape[1])
+        _write(a.out, _host(rk.backprojection(g, _to_dev(sino), rk.ProjectorOptions(a.step))))
+        return 0
+    if a.cmd == "filter":  # cli.cpp:310-318
+        sino = _read(a.inp, 3)
+        _write(a.out, _host(rk.filter_sinogram(_to_dev(sino), rk.make_filter(a.filter, sino.shape[2]))))
+        return 0
+    if a.cmd == "fbp":  # cli.cpp:338-358
+        sino = _apply_precision(_read(a.inp, 3), a.precision)
+        if a.det_count == 0:
+            a.det_count = sino.shape[2]
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else sino.shape[1])
+        t0 = time.perf_counter()
+        rec = _host(rk.fbp(g, _to_dev(sino), a.filter))
+        secs = time.perf_counter() - t0
+        _write(a.out, rec)
+        rep = {"command": "fbp", "filter": a.filter, "seconds": secs, "geometry": geometry_json(g), "output": a.out}
+        if a.reference:
+            ref = np.load(a.reference).astype(np.float64)
+            rep["mse_vs_reference"] = float(np.mean((rec.reshape(ref.shape).astype(np.float64) - ref) ** 2))
+        if a.json:
+            print(json.dumps(rep, indent=2))
+        elif a.reference:
+            print(f"mse vs reference: {rep['mse_vs_reference']:.6e}")
+        return 0
+    if a.cmd == "solve":  # cli.cpp:397-437
+        sino = _apply_precision(_read(a.inp, 3), a.precision)
+        if a.det_count == 0:
+            a.det_count = sino.shape[2]
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else sino.shape[1])
+        op = rk.projector_operator(g, rk.ProjectorOptions(a.step))
+        y = _to_dev(sino)
+        guess = torch.zeros((y.shape[0], a.size, a.size), dtype=y.dtype, device=y.device)
+        t0 = time.perf_counter()
+        alpha = None
+        if a.method == "landweber":
+            alpha = a.alpha if a.alpha > 0 else 0.95 * rk.estimate_alpha(op, a.alpha_iterations, a.seed)
+            x = rk.landweber(op, y, guess, alpha, a.iterations)
+        elif a.method == "cgne":
+            x = rk.cgne(op, guess, y, a.iterations, a.tolerance)
+        else:
+            b = op.adjoint(y)
+            x = rk.cg(lambda v: op.adjoint(op.apply(v)), guess, b, a.iterations, a.tolerance)
+        rec = _host(x)
+        secs = time.perf_counter() - t0
+        _write(a.out, rec)
+        rep = {"command": "solve", "method": a.method, "iterations": a.iterations, "seconds": secs,
+               "geometry": geometry_json(g), "output": a.out}
+        if alpha is not None:
+            rep["alpha"] = alpha
+        if a.reference:
+            ref = np.load(a.reference).astype(np.float64)
+            rep["mse_vs_reference"] = float(np.mean((rec.reshape(ref.shape).astype(np.float64) - ref) ** 2))
+        if a.json:
+            print(json.dumps(rep, indent=2))
+        return 0
+    if a.cmd == "check-adjoint":  # cli.cpp:581-616
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else a.size)
+        d = rk.adjoint_check(rk.projector_operator(g, rk.ProjectorOptions(a.step)), a.trials, a.seed)
+        if a.json:
+            rep = {"command": "check-adjoint", "operator": "projector", "defect": d, "trials": a.trials,
+                   "seed": a.seed, "detail": geometry_json(g)}
+            if a.tolerance > 0:
+                rep["tolerance"] = a.tolerance
+            print(json.dumps(rep, indent=2))
+        else:
+            print(f"adjoint defect: {d:.6e}")
+        if a.tolerance > 0 and not (d <= a.tolerance):
+            print(f"adjoint defect {d:.6e} exceeds tolerance {a.tolerance:.6e}", file=sys.stderr)
+            return 2
+        return 0
+    if a.cmd == "bench":  # cli.cpp:619-689 (device-timed per call, median)
+        if a.runs < 5:
+            raise ValidationError("--runs must be >= 5")
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else a.size)
+        from .phantom import shepp_logan
+
+        one = shepp_logan(a.size)
+        img = torch.from_numpy(np.repeat(one[None], a.batch, 0).astype(_PREC[a.precision])).cuda()
+        opts = rk.ProjectorOptions(a.step)
+        sino = rk.forward(g, img, opts)
+
+        def time_op(fn):
+            for _ in range(a.warmup):
+                fn()
+            runs = []
+            for _ in range(a.runs):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                runs.append(e0.elapsed_time(e1))
+            med = float(np.median(runs))
+            return {"median_ms": med, "images_per_s": a.batch / (med / 1000.0), "runs_ms": runs}
+
+        fwd = time_op(lambda: rk.forward(g, img, opts))
+        bwd = time_op(lambda: rk.backprojection(g, sino, opts))
+        rep = {"version": VERSION, "geometry": geometry_json(g), "batch": a.batch, "precision": a.precision,
+               "warmup": a.warmup, "runs": a.runs, "threads": 1, "device": torch.cuda.get_device_name(),
+               "forward": fwd, "backprojection": bwd}
+        if a.json:
+            print(json.dumps(rep, indent=2))
+        else:
+            print(f"{VERSION}\nforward: {fwd['median_ms']:.3f} ms/call median, {fwd['images_per_s']:.2f} images/s")
+            print(f"backprojection: {bwd['median_ms']:.3f} ms/call median, {bwd['images_per_s']:.2f} images/s")
+        return 0
+    return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
