@@ -225,7 +225,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
 
   // Per-CTA layout by simulation, then greedy chunks (parallel over CTAs).
   struct CtaPlan {
-    int tr = 0, residue = 0, swap = 0;
+    int tr = 0, residue = 0, swap = 0, mapping = 0;
     bool ok = false;
     int64_t staged = 0, max_cells = 0;
     std::vector<int4> boxes;
@@ -240,31 +240,51 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
         const int2* wa = &warps[size_t(cta) * 8];
         CtaPlan& cp = plans[size_t(cta)];
         // lane positions at a few aligned steps of the march
-        sim.clear();
-        for (int st = 0; st < 4; ++st) {
-          const double tt = t_lo + (t_hi - t_lo) * (0.2 + 0.6 * double(st) / 3.0);
-          for (int w = 0; w < 8; ++w)
-            for (int l = 0; l < 32; ++l) {
-              Pt q{NAN, NAN};
-              const int64_t kk = int64_t(wa[w].y) + l;
-              if (wa[w].x >= 0 && kk < nd) {
-                const RayD& ry = rays[size_t(int64_t(wa[w].x) * nd + kk)];
-                if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
-                  const double m = std::floor((tt - ry.t0) / ry.h);
-                  const double t = ry.t0 + (m + 0.5) * ry.h;
-                  q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
-                }
-              }
-              sim.push_back(q);
-            }
-        }
+        // Two lane mappings: detector-major (warp = one angle, lanes = 32 cells) and,
+        // for a full 8-angle x 32-cell CTA, angle-major (warp w = cells 4w..4w+3,
+        // lane l = angle slot l & 7, cell 4w + l / 8): a quarter warp then reads
+        // one cell's 8 neighbouring angles, points on a short arc that often share
+        // texels.  Positions at a few aligned steps of the march, in lane order.
+        const bool full8 = sh.aa == 8 && sh.db == 1;
+        auto lane_ray = [&](int mapping, int w, int l, int& a_out, int64_t& k_out) {
+          if (mapping == 0) {
+            a_out = wa[w].x;
+            k_out = int64_t(wa[w].y) + l;
+          } else {
+            a_out = wa[l & 7].x;
+            k_out = int64_t(wa[0].y) + 4 * w + (l >> 3);
+          }
+        };
         double best = 1e300;
-        for (int tr = 0; tr < 2; ++tr)
-          for (int swap = 0; swap < 3; ++swap)
-            for (int res = 0; res < 8; ++res) {
-              const double c = conflict_cost(sim, tr == 1, 64 + res, swap) * (1.0 + 1e-3 * tr + 1e-5 * swap);
-              if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap;
-            }
+        for (int mapping = 0; mapping < (full8 ? 2 : 1); ++mapping) {
+          sim.clear();
+          for (int st = 0; st < 8; ++st) {
+            const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st) / 7.0);
+            for (int w = 0; w < 8; ++w)
+              for (int l = 0; l < 32; ++l) {
+                Pt q{NAN, NAN};
+                int a;
+                int64_t kk;
+                lane_ray(mapping, w, l, a, kk);
+                if (a >= 0 && kk < nd) {
+                  const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
+                  if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
+                    const double m = std::floor((tt - ry.t0) / ry.h);
+                    const double t = ry.t0 + (m + 0.5) * ry.h;
+                    q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
+                  }
+                }
+                sim.push_back(q);
+              }
+          }
+          for (int tr = 0; tr < 2; ++tr)
+            for (int swap = 0; swap < 3; ++swap)
+              for (int res = 0; res < 8; ++res) {
+                const double c = conflict_cost(sim, tr == 1, 64 + res, swap) *
+                                 (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
+                if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap, cp.mapping = mapping;
+              }
+        }
         cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
       }
     };
@@ -306,15 +326,16 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     F.any_transposed = false;
     for (size_t c = 0; c < plans.size(); ++c) {
       const CtaPlan& cp = plans[c];
-      F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()), cp.tr | (cp.swap << 1), 0);
+      F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()), cp.tr | (cp.swap << 1) | (cp.mapping << 3), 0);
       F.boxes.insert(F.boxes.end(), cp.boxes.begin(), cp.boxes.end());
       F.max_box = std::max(F.max_box, cp.max_cells);
       F.staged_texels += cp.staged;
       F.any_transposed |= cp.tr == 1;
     }
     if (std::getenv("RK_DEBUG_PLAN")) {
-      int64_t ntr = 0;
-      for (const int4& c : F.cta) ntr += c.z & 1;
+      int64_t ntr = 0, nam = 0;
+      for (const int4& c : F.cta) ntr += c.z & 1, nam += (c.z >> 3) & 1;
+      std::fprintf(stderr, "[rk] forward schedule: %lld CTAs angle-major\n", (long long)nam);
       std::fprintf(stderr,
                    "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
                    "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",

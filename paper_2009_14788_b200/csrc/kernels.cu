@@ -135,11 +135,16 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
   const int cta = blockIdx.x;
   const int64_t g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int2 wa = __ldg(warps + cta * (kFwdThreads / 32) + warp);  // {angle, first cell}; angles sorted by direction
-  const int a = wa.x, k = wa.y + lane;
+  const int4 cfg = __ldg(cta_cfg + cta);  // {first box, boxes, flags}
+  // lane -> ray: detector-major (warp = angle slot, lane = cell) or angle-major
+  // (lane & 7 = angle slot, cell 4 warp + lane / 8), chosen by the planner
+  // against bank conflicts; angles are sorted by direction
+  const bool amaj = ((cfg.z >> 3) & 1) != 0;
+  const int2 wa = __ldg(warps + cta * (kFwdThreads / 32) + (amaj ? (lane & 7) : warp));
+  const int a = wa.x;
+  const int k = amaj ? __ldg(warps + cta * (kFwdThreads / 32)).y + 4 * warp + (lane >> 3) : wa.y + lane;
   const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
-  const int4 cfg = __ldg(cta_cfg + cta);  // {first box, boxes, flags}
   const bool tr = (cfg.z & 1) != 0;
   // Per-lane tap order chosen by the planner against bank conflicts: odd lanes
   // issue the bottom row first (swap 1) or the right column first (swap 2).
