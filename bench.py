@@ -309,8 +309,16 @@ def main():
     dom, dbytes, dms = ("forward", fwd_bytes, fwd_ms) if fwd_ms >= bp_ms else ("backproject", bp_bytes, bp_ms)
     achieved = dbytes / (dms * 1e-3) / 1e9
     peak = float(smem_peak.value)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        rec = json.load(open(tfile)).get(args.workload, {}).get(dom)
+        if rec:  # DRAM bytes per launch from the committed ncu --set full capture, rescaled to this batch
+            traffic = rec["bytes_per_image"] * nb
     roofline = {"bound": "l1tex", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/ncu_traffic.json); "
+                                "HBM is not the binding resource: the kernel's data path is shared memory",
                 "peak_source": "measured in this run by rk_probe_smem_bandwidth (LDS.128, all SMs); "
                                "MEASURED_PEAKS.json has no L1TEX/SMEM figure",
                 "algorithmic_bytes_per_launch": dbytes,
