@@ -105,11 +105,37 @@ __global__ void transpose_images_kernel(const float4* __restrict__ src, int P, f
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// one row of the staged box: `bytes` (multiple of 16) from global to shared
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (lanes)
 
@@ -117,7 +143,8 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // 8 angles x 32 detector cells and per packed group of four images.  All rays
 // of the CTA march together chunk by chunk along t; before each chunk the
 // box of padded-image texels its samples can touch (fwd_plan.cpp) is copied
-// to shared memory with cp.async, then each lane runs its own samples of the
+// to shared memory by TMA bulk copies (one per box row, completing on an
+// mbarrier), then each lane runs its own samples of the
 // chunk: sample m at (px0, py0) + (m + 0.5) (hx, hy) — the reference's
 // t_m = t0 + (m + 0.5) h — bilinear taps as four 128-bit shared loads (one
 // tap of four images each), weights shared by the four images.  Samples are
@@ -132,6 +159,7 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
     const int2* __restrict__ warps, int na, int nd, int64_t batch, TOut* __restrict__ sino, FwdEpilogue epi) {
   extern __shared__ float4 box_s[];
+  __shared__ unsigned long long box_bar;  // TMA completion of the current chunk's box
   const int cta = blockIdx.x;
   const int64_t g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,6 +195,11 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
   const float4* src = (tr ? img_t : img) + g * int64_t(P) * P;
   const int4* bxs = boxes + cfg.x;
 
+  if (threadIdx.x == 0) {
+    mbar_init(&box_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   int m = 0;
   for (int c = 0; c < cfg.y; ++c) {
@@ -177,13 +210,14 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const int m_end =
         isinf(tend) ? n : min(max(int(ceilf(fmaf(tend - t0, inv_h, -0.5f))), 0), n);
     __syncthreads();  // previous chunk's samples are done with the box
-    for (int rr = warp; rr < rows; rr += kFwdThreads / 32) {
-      const float4* srow = src + int64_t(r0 + rr) * P + c0;
-      float4* drow = box_s + rr * pitch;
-      for (int cc = lane; cc < cols; cc += 32) cp_async16(drow + cc, srow + cc);
+    // stage the box: one TMA bulk copy per row (warp 0), completion on the mbarrier
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(&box_bar, unsigned(rows * cols) * 16u);
+      __syncwarp();
+      for (int rr = lane; rr < rows; rr += 32)
+        tma_bulk_g2s(box_s + rr * pitch, src + int64_t(r0 + rr) * P + c0, unsigned(cols) * 16u, &box_bar);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    mbar_wait(&box_bar, unsigned(c & 1));
     const float ox = float(c0), oy = float(r0);
     const int jmax = cols - 2, imax = rows - 2;
     const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
