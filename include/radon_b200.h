@@ -169,6 +169,27 @@ int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess,
 int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter,
             double tolerance, void* d_x, int* failed_iteration, void* stream);
 
+/* ------------------------------------------------------------- shearlets + ADMM */
+typedef struct rk_shearlet rk_shearlet;
+/* make_plan (shearlet.hpp:37): cone-adapted alpha-shearlet Fourier multipliers,
+ * Parseval-normalised; power-of-two square grids on the device.  device -1:
+ * host-only (multipliers for inspection). */
+int rk_shearlet_create(int64_t height, int64_t width, const double* alphas, int n_scales, int device,
+                       rk_shearlet** plan);
+/* make_plan_cached (shearlet.hpp:43, shearlet.cpp:201-249): a plan over stored
+ * n_coeff x h x w fp64 multipliers (the cache file's payload), used verbatim. */
+int rk_shearlet_create_stored(int64_t height, int64_t width, const double* alphas, int n_scales,
+                              const double* multipliers, int device, rk_shearlet** plan);
+int rk_shearlet_destroy(rk_shearlet* plan);
+/* n_coeff; scales (n_coeff labels, may be NULL); multipliers (n_coeff x h x w fp64, may be NULL). */
+int rk_shearlet_info(const rk_shearlet* plan, int64_t* n_coeff, double* scales, double* multipliers);
+/* forward(plan, image): batch x h x w -> batch x n_coeff x h x w (shearlet.hpp:49). */
+int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64_t batch, void* d_coeff,
+                        void* stream);
+/* backward(plan, coeff): batch x n_coeff x h x w -> batch x h x w, exact adjoint (shearlet.hpp:51). */
+int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int64_t batch, void* d_image,
+                         void* stream);
+
 /* ------------------------------------------------------------- instrumentation (no reference equivalent) */
 typedef enum {
   RK_KERNEL_PACK = 0,        /* layout packing (image / sinogram -> 4-image interleave) */
@@ -176,7 +197,8 @@ typedef enum {
   RK_KERNEL_BACKPROJECT = 2, /* pixel-driven backprojector                               */
   RK_KERNEL_FILTER = 3,      /* ramp filter                                              */
   RK_KERNEL_SOLVER = 4,      /* fused solver vector kernels / reductions                 */
-  RK_KERNEL_KINDS = 5
+  RK_KERNEL_SHEARLET = 5,    /* shearlet 2-D FFT passes / ADMM updates                    */
+  RK_KERNEL_KINDS = 6
 } rk_kernel_kind;
 
 typedef struct rk_kernel_stats {

@@ -241,6 +241,63 @@ class RefOracle:
     def float_to_half_bits(self, f: float) -> int:
         return int(self.lib.ref_float_to_half(float(f)))
 
+    # --- shearlets (shearlet.cpp:103-330) and ADMM (admm.cpp:111-163), SURVEY 8f ranks 3-4 ---
+    @staticmethod
+    def _alphas(alphas):
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        return a, len(a)
+
+    def shearlet_n_coeff(self, h: int, w: int, alphas) -> int:
+        a, n = self._alphas(alphas)
+        nc = ctypes.c_int64()
+        self._check(self.lib.ref_shearlet_plan(ctypes.c_int64(h), ctypes.c_int64(w), _ptr(a), n, ctypes.byref(nc),
+                                               None, None))
+        return int(nc.value)
+
+    def shearlet_plan(self, h: int, w: int, alphas):
+        """(n_coeff, scales[n_coeff], multipliers[n_coeff, h, w]) as make_plan builds them."""
+        a, n = self._alphas(alphas)
+        nc = ctypes.c_int64()
+        self._check(self.lib.ref_shearlet_plan(ctypes.c_int64(h), ctypes.c_int64(w), _ptr(a), n, ctypes.byref(nc),
+                                               None, None))
+        scales = np.empty(nc.value, np.float64)
+        mult = np.empty((nc.value, h, w), np.float64)
+        self._check(self.lib.ref_shearlet_plan(ctypes.c_int64(h), ctypes.c_int64(w), _ptr(a), n, ctypes.byref(nc),
+                                               _ptr(scales), _ptr(mult)))
+        return int(nc.value), scales, mult
+
+    def shearlet_forward(self, image: np.ndarray, alphas) -> np.ndarray:
+        image = np.ascontiguousarray(image)
+        B, h, w = image.shape
+        nc = self.shearlet_n_coeff(h, w, alphas)
+        a, n = self._alphas(alphas)
+        out = np.empty((B, nc, h, w), image.dtype)
+        self._check(self.lib.ref_shearlet_forward(ctypes.c_int64(h), ctypes.c_int64(w), _ptr(a), n,
+                                                  _PREC[image.dtype], ctypes.c_int64(B), _ptr(image), _ptr(out)))
+        return out
+
+    def shearlet_backward(self, coeff: np.ndarray, alphas) -> np.ndarray:
+        coeff = np.ascontiguousarray(coeff)
+        B, nc, h, w = coeff.shape
+        a, n = self._alphas(alphas)
+        out = np.empty((B, h, w), coeff.dtype)
+        self._check(self.lib.ref_shearlet_backward(ctypes.c_int64(h), ctypes.c_int64(w), _ptr(a), n,
+                                                   _PREC[coeff.dtype], ctypes.c_int64(B), _ptr(coeff), _ptr(out)))
+        return out
+
+    def admm(self, g: Geom, sino: np.ndarray, alphas, p0: float, p1: float, outer: int, inner: int,
+             weights=None) -> np.ndarray:
+        sino = np.ascontiguousarray(sino)
+        a, n = self._alphas(alphas)
+        wts = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+        out = np.empty((sino.shape[0], g.image_size, g.image_size), sino.dtype)
+        c, keep = self._geom(g)
+        self._check(self.lib.ref_admm(ctypes.byref(c), _ptr(a), n, _PREC[sino.dtype], ctypes.c_int64(sino.shape[0]),
+                                      _ptr(sino), ctypes.c_double(p0), ctypes.c_double(p1),
+                                      None if wts is None else _ptr(wts), ctypes.c_int64(outer),
+                                      ctypes.c_int64(inner), _ptr(out)))
+        return out
+
 
 def _narrow(d: np.ndarray, dtype) -> np.ndarray:
     """Tensor::from_double_as (tensor.cpp:111-124): double -> storage, half via float."""

@@ -7,7 +7,8 @@
 // FFTW's published semantics (proj/core/include/radonkit/fft.hpp:8-14):
 //   rfft : n reals -> n/2+1 complex bins, unnormalised forward transform
 //   irfft: n/2+1 bins (Hermitian half spectrum) -> n reals, scaled by 1/n
-// The 2D transforms (shearlet-only, out of scope) throw.
+// The 2D transforms (shearlets) use the same 1-D FFT
+// along rows then columns.
 //
 // Algorithm (both precisions): iterative radix-2 decimation-in-time FFT of
 // the real row embedded as complex, twiddles W_n^k = exp(-/+ 2 pi i k / n)
@@ -139,9 +140,56 @@ void irfft(int n, const std::complex<double>* in, double* out) {
   for (int i = 0; i < n; ++i) out[i] = a[size_t(i)].real() * inv;
 }
 
-void rfft2(int, int, const float*, std::complex<float>*) { throw std::logic_error("rfft2: out of oracle scope"); }
-void irfft2(int, int, const std::complex<float>*, float*) { throw std::logic_error("irfft2: out of oracle scope"); }
-void rfft2(int, int, const double*, std::complex<double>*) { throw std::logic_error("rfft2: out of oracle scope"); }
-void irfft2(int, int, const std::complex<double>*, double*) { throw std::logic_error("irfft2: out of oracle scope"); }
+// 2-D transforms (shearlet.cpp's rfft2 / irfft2): row transforms then column
+// transforms with the same 1-D FFT, in the working precision; h x (w/2+1) half
+// spectrum; the inverse keeps FFTW's c2r semantics (Hermitian completion of
+// every row, 1/(h w) normalisation).
+namespace {
+template <class T>
+void rfft2_t(int h, int w, const T* in, std::complex<T>* out) {
+  const int wc = w / 2 + 1;
+  std::vector<std::complex<T>> full(static_cast<size_t>(h) * static_cast<size_t>(w));
+  std::vector<std::complex<T>> row(static_cast<size_t>(w));
+  for (int i = 0; i < h; ++i) {
+    for (int j = 0; j < w; ++j) row[size_t(j)] = {in[size_t(i) * w + j], T(0)};
+    cfft(row, +1);
+    for (int j = 0; j < w; ++j) full[size_t(i) * w + j] = row[size_t(j)];
+  }
+  std::vector<std::complex<T>> col(static_cast<size_t>(h));
+  for (int j = 0; j < wc; ++j) {
+    for (int i = 0; i < h; ++i) col[size_t(i)] = full[size_t(i) * w + j];
+    cfft(col, +1);
+    for (int i = 0; i < h; ++i) out[size_t(i) * wc + j] = col[size_t(i)];
+  }
+}
+
+template <class T>
+void irfft2_t(int h, int w, const std::complex<T>* in, T* out) {
+  const int wc = w / 2 + 1;
+  // inverse along columns on the half spectrum, then a c2r row transform
+  std::vector<std::complex<T>> half(static_cast<size_t>(h) * static_cast<size_t>(wc));
+  std::vector<std::complex<T>> col(static_cast<size_t>(h));
+  for (int j = 0; j < wc; ++j) {
+    for (int i = 0; i < h; ++i) col[size_t(i)] = in[size_t(i) * wc + j];
+    cfft(col, -1);
+    for (int i = 0; i < h; ++i) half[size_t(i) * wc + j] = col[size_t(i)];
+  }
+  std::vector<std::complex<T>> row(static_cast<size_t>(w));
+  const T inv = T(1) / (T(h) * T(w));
+  for (int i = 0; i < h; ++i) {
+    for (int q = 0; q < wc; ++q) row[size_t(q)] = half[size_t(i) * wc + q];
+    for (int q = wc; q < w; ++q) row[size_t(q)] = std::conj(half[size_t(i) * wc + (w - q)]);
+    row[0] = {row[0].real(), T(0)};
+    if (w % 2 == 0) row[size_t(w / 2)] = {row[size_t(w / 2)].real(), T(0)};
+    cfft(row, -1);
+    for (int j = 0; j < w; ++j) out[size_t(i) * w + j] = row[size_t(j)].real() * inv;
+  }
+}
+}  // namespace
+
+void rfft2(int h, int w, const float* in, std::complex<float>* out) { rfft2_t(h, w, in, out); }
+void irfft2(int h, int w, const std::complex<float>* in, float* out) { irfft2_t(h, w, in, out); }
+void rfft2(int h, int w, const double* in, std::complex<double>* out) { rfft2_t(h, w, in, out); }
+void irfft2(int h, int w, const std::complex<double>* in, double* out) { irfft2_t(h, w, in, out); }
 
 }  // namespace radonkit::fft

@@ -15,12 +15,14 @@
 #include <string>
 #include <vector>
 
+#include "radonkit/admm.hpp"
 #include "radonkit/errors.hpp"
 #include "radonkit/geometry.hpp"
 #include "radonkit/linop.hpp"
 #include "radonkit/phantom.hpp"
 #include "radonkit/projector.hpp"
 #include "radonkit/rng.hpp"
+#include "radonkit/shearlet.hpp"
 #include "radonkit/sino_filter.hpp"
 #include "radonkit/solvers.hpp"
 #include "radonkit/tensor.hpp"
@@ -251,6 +253,53 @@ int ref_cgne(const RefGeom* g, int prec, int64_t batch, const void* y, const voi
 }
 
 // half.hpp:12-71
+// shearlet.cpp:103-198 (make_plan): n_coeff, scale labels, fp64 multipliers
+int ref_shearlet_plan(int64_t h, int64_t w, const double* alphas, int n_scales, int64_t* n_coeff, double* scales,
+                      double* multipliers) {
+  return guard([&] {
+    ShearletPlan p = make_plan(h, w, std::vector<double>(alphas, alphas + n_scales));
+    *n_coeff = p.n_coeff;
+    if (scales) std::memcpy(scales, p.scales.data(), p.scales.size() * 8);
+    if (multipliers) std::memcpy(multipliers, p.multipliers.data(), p.multipliers.size() * 8);
+  });
+}
+
+// shearlet.cpp:296-311 (forward: B x h x w -> B x n_coeff x h x w)
+int ref_shearlet_forward(int64_t h, int64_t w, const double* alphas, int n_scales, int prec, int64_t batch,
+                         const void* image, void* coeff) {
+  return guard([&] {
+    ShearletPlan p = make_plan(h, w, std::vector<double>(alphas, alphas + n_scales));
+    store(forward(p, make_tensor({batch, h, w}, prec_of(prec), image)), coeff);
+  });
+}
+
+// shearlet.cpp:313-330 (backward: B x n_coeff x h x w -> B x h x w)
+int ref_shearlet_backward(int64_t h, int64_t w, const double* alphas, int n_scales, int prec, int64_t batch,
+                          const void* coeff, void* image) {
+  return guard([&] {
+    ShearletPlan p = make_plan(h, w, std::vector<double>(alphas, alphas + n_scales));
+    store(backward(p, make_tensor({batch, p.n_coeff, h, w}, prec_of(prec), coeff)), image);
+  });
+}
+
+// admm.cpp:111-163 (default weights 3^scale / 400 when weights == NULL)
+int ref_admm(const RefGeom* g, const double* alphas, int n_scales, int prec, int64_t batch, const void* sino,
+             double p0, double p1, const double* weights, int64_t outer, int64_t inner, void* image) {
+  return guard([&] {
+    Geometry geo = build(g);
+    const int64_t s = geometry_image_size(geo);
+    ShearletPlan plan = make_plan(s, s, std::vector<double>(alphas, alphas + n_scales));
+    AdmmParams prm;
+    prm.p0 = p0;
+    prm.p1 = p1;
+    prm.outer_iterations = outer;
+    prm.inner_cg_iterations = inner;
+    if (weights) prm.weights = Tensor::from_vec({1, plan.n_coeff, 1, 1}, std::vector<double>(weights, weights + plan.n_coeff));
+    Tensor y = make_tensor({batch, geometry_n_angles(geo), geometry_det_count(geo)}, prec_of(prec), sino);
+    store(admm_reconstruct(projector_operator(geo, ProjectorOptions{g->step}), plan, y, prm), image);
+  });
+}
+
 uint16_t ref_float_to_half(float f) { return float_to_half(f); }
 float ref_half_to_float(uint16_t h) { return half_to_float(h); }
 

@@ -13,11 +13,24 @@ from .errors import (CudaError, DivergenceError, HalfOverflowError, NotPositiveD
                      ValidationError)
 from .geometry import (FanbeamGeometry, Geometry, ParallelGeometry, angles_linspace, geometry_det_count,
                        geometry_image_size, geometry_n_angles, make_fanbeam, make_parallel)
-from .projector import ProjectorOptions, backprojection, forward, get_plan
+from .projector import ProjectorOptions, backprojection, get_plan
+from .projector import forward as _projector_forward
 from .sino_filter import FilterKind, FilterSpec, fbp, filter_kind_from_name, filter_kind_name, filter_sinogram, make_filter
 from .linop import (LinearOperator, adjoint_check, compose, gradient_check, identity_operator, projector_operator)
 from .rng import Rng
 from .solvers import cg, cgne, estimate_alpha, landweber
+from . import shearlet
+from .shearlet import ShearletPlan, backward, make_plan, make_plan_cached, shearlet_operator
+
+
+def forward(plan_or_geometry, x, *args, **kwargs):
+    """The reference's two ``forward`` overloads: Radon projection
+    (projector.hpp, ``forward(geometry, image[, opts])``) and shearlet analysis
+    (shearlet.hpp:49, ``forward(plan, image)``)."""
+    if isinstance(plan_or_geometry, ShearletPlan):
+        return shearlet.forward(plan_or_geometry, x, *args, **kwargs)
+    return _projector_forward(plan_or_geometry, x, *args, **kwargs)
+
 
 __all__ = [
     "CudaError", "DivergenceError", "HalfOverflowError", "NotPositiveDefiniteError", "NumericalError",
@@ -26,4 +39,5 @@ __all__ = [
     "backprojection", "forward", "get_plan", "FilterKind", "FilterSpec", "fbp", "filter_kind_from_name",
     "filter_kind_name", "filter_sinogram", "make_filter", "LinearOperator", "adjoint_check", "compose",
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
+    "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",
 ]

@@ -72,16 +72,22 @@ SIGNATURES = {
     "rk_estimate_alpha": (_i, [_vp, _i, _u64, _P(_d)]),
     "rk_landweber": (_i, [_vp, _i, _vp, _vp, _i64, _d, _i, _vp, _P(_i), _vp]),
     "rk_cgne": (_i, [_vp, _i, _vp, _vp, _i64, _i, _d, _vp, _P(_i), _vp]),
+    "rk_shearlet_create": (_i, [_i64, _i64, _vp, _i, _i, _P(_vp)]),
+    "rk_shearlet_create_stored": (_i, [_i64, _i64, _vp, _i, _vp, _i, _P(_vp)]),
+    "rk_shearlet_destroy": (_i, [_vp]),
+    "rk_shearlet_info": (_i, [_vp, _P(_i64), _vp, _vp]),
+    "rk_shearlet_forward": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
+    "rk_shearlet_backward": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
     "rk_profiling_enable": (_i, [_i]),
     "rk_profiling_read": (_i, [_vp, _i]),  # (rk_kernel_stats*, reset): pass ctypes.byref(RkKernelStats())
     "rk_probe_smem_bandwidth": (_i, [_i, _P(_d)]),
 }
 
-KERNEL_KINDS = ["pack", "forward", "backproject", "filter", "solver"]
+KERNEL_KINDS = ["pack", "forward", "backproject", "filter", "solver", "shearlet"]
 
 
 class RkKernelStats(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 5), ("timed", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5)]
+    _fields_ = [("launches", ctypes.c_int64 * 6), ("timed", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6)]
 
 
 def _load() -> ctypes.CDLL:

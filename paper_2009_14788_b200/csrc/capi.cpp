@@ -437,6 +437,93 @@ int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int6
   });
 }
 
+int rk_shearlet_create(int64_t height, int64_t width, const double* alphas, int n_scales, int device,
+                       rk_shearlet** plan) {
+  return guarded([&] {
+    require(plan != nullptr, "plan pointer is null");
+    require(alphas != nullptr || n_scales == 0, "alphas pointer is null");
+    *plan = nullptr;
+    auto hs = std::make_unique<rk_shearlet>();
+    hs->s.device = device;
+    if (device >= 0) {
+      int count = 0;
+      RK_CUDA(cudaGetDeviceCount(&count));
+      require(device < count, "device " + std::to_string(device) + " out of range");
+    }
+    rk::build_shearlet(hs->s, height, width, std::vector<double>(alphas, alphas + std::max(n_scales, 0)));
+    *plan = hs.release();
+  });
+}
+
+int rk_shearlet_create_stored(int64_t height, int64_t width, const double* alphas, int n_scales,
+                              const double* multipliers, int device, rk_shearlet** plan) {
+  return guarded([&] {
+    require(plan != nullptr, "plan pointer is null");
+    require(alphas != nullptr || n_scales == 0, "alphas pointer is null");
+    require(multipliers != nullptr, "multipliers pointer is null");
+    *plan = nullptr;
+    auto hs = std::make_unique<rk_shearlet>();
+    hs->s.device = device;
+    if (device >= 0) {
+      int count = 0;
+      RK_CUDA(cudaGetDeviceCount(&count));
+      require(device < count, "device " + std::to_string(device) + " out of range");
+    }
+    rk::build_shearlet(hs->s, height, width, std::vector<double>(alphas, alphas + std::max(n_scales, 0)),
+                       multipliers);
+    *plan = hs.release();
+  });
+}
+
+int rk_shearlet_destroy(rk_shearlet* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    if (plan->s.device >= 0) {
+      cudaSetDevice(plan->s.device);
+      cudaDeviceSynchronize();
+    }
+    delete plan;
+  });
+}
+
+int rk_shearlet_info(const rk_shearlet* plan, int64_t* n_coeff, double* scales, double* multipliers) {
+  return guarded([&] {
+    require(plan != nullptr, "plan is null");
+    const rk::Shearlet& s = plan->s;
+    if (n_coeff) *n_coeff = s.n_coeff;
+    if (scales) std::memcpy(scales, s.scales.data(), s.scales.size() * sizeof(double));
+    if (multipliers) std::memcpy(multipliers, s.multipliers.data(), s.multipliers.size() * sizeof(double));
+  });
+}
+
+// shearlet.cpp:296-311
+int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64_t batch, void* d_coeff,
+                        void* stream) {
+  return guarded([&] {
+    require(plan != nullptr && plan->s.device >= 0, "shearlet plan is null or host-only");
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
+    std::lock_guard<std::mutex> lock(plan->s.mu);
+    RK_CUDA(cudaSetDevice(plan->s.device));
+    rk::shearlet_forward(plan->s, dtype, d_image, batch, d_coeff, as_stream(stream));
+  });
+}
+
+// shearlet.cpp:313-330
+int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int64_t batch, void* d_image,
+                         void* stream) {
+  return guarded([&] {
+    require(plan != nullptr && plan->s.device >= 0, "shearlet plan is null or host-only");
+    check_dtype(dtype);
+    require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+    require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
+    std::lock_guard<std::mutex> lock(plan->s.mu);
+    RK_CUDA(cudaSetDevice(plan->s.device));
+    rk::shearlet_backward(plan->s, dtype, d_coeff, batch, d_image, as_stream(stream));
+  });
+}
+
 int rk_profiling_enable(int enable) {
   return guarded([&] { rk::profiling_enable(enable != 0); });
 }

@@ -136,6 +136,31 @@ struct Filter {
   std::mutex mu;
 };
 
+// Alpha-shearlet frame (shearlet_plan.cpp / shearlet.cu; reference shearlet.cpp)
+struct Shearlet {
+  int device = 0;
+  int64_t height = 0, width = 0, n_coeff = 0;
+  std::vector<double> alphas, scales;
+  std::vector<double> multipliers;  // n_coeff x h x w (fp64, natural layout)
+  DeviceBuffer d_mult_t;            // fp32, per coefficient transposed (column-major) grid
+  DeviceBuffer d_twiddle;           // float2, h/2 forward twiddles
+  DeviceBuffer d_mult_t64, d_twiddle64;  // fp64 copies for fp64 storage (built on first use)
+  DeviceBuffer work_a, work_b;      // spectra scratch
+  std::mutex mu;
+};
+// stored != nullptr: n_coeff x h x w multipliers from a plan cache, used verbatim
+void build_shearlet(Shearlet& sp, int64_t height, int64_t width, const std::vector<double>& alphas,
+                    const double* stored = nullptr);
+void upload_shearlet(Shearlet& sp);
+void shearlet_forward(Shearlet& sp, int dtype, const void* image, int64_t batch, void* coeff, cudaStream_t st);
+void shearlet_backward(Shearlet& sp, int dtype, const void* coeff, int64_t batch, void* image, cudaStream_t st);
+// ADMM fusions (fp32, user layouts): z1 = shrink(SH(f) + u1, thresh_k), u1 += SH(f) - z1
+// (non-finite u1 -> atomicMin(flag, iteration)); image = SH'(z1 - u1)
+void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1, float* u1, const float* thresh,
+                          int* flag, int iteration, cudaStream_t st);
+void shearlet_admm_synth(Shearlet& sp, const float* z1, const float* u1, int64_t batch, float* image,
+                         cudaStream_t st);
+
 // ----------------------------------------------------------------- host helpers (plan.cpp)
 rk_geometry resolve_geometry(const rk_geometry& in);
 void build_plan(Plan& p);
@@ -217,4 +242,7 @@ struct rk_plan {
 };
 struct rk_filter {
   rk::Filter f;
+};
+struct rk_shearlet {
+  rk::Shearlet s;
 };
