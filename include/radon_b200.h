@@ -190,6 +190,26 @@ int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64
 int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int64_t batch, void* d_image,
                          void* stream);
 
+/* admm_reconstruct (admm.hpp:49-50, admm.cpp:111-163): l1-shearlet ADMM with a
+ * positivity split; CG on (p0 A'A + (1 + p1) I) warm-started from the previous
+ * f, `inner_cg_iterations` steps per outer iteration.  weights: n_coeff values,
+ * NULL = 3^scale / 400 (admm.cpp:11-15).  fp32 state for every storage dtype.
+ * The shearlet grid must equal the projector's image grid.  A non-finite state
+ * returns RK_ERR_NUMERICAL (DivergenceError) with *failed_iteration set. */
+int rk_admm(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0, double p1,
+            const double* weights, int64_t outer_iterations, int inner_cg_iterations, void* d_image,
+            int64_t* failed_iteration, void* stream);
+/* Stepwise form (the reference's AdmmObserver, admm.hpp:33-34): create computes
+ * bp = A'y and the zero state; iterate runs n outer iterations; read copies one
+ * state variable (0 f, 1 z1, 2 u1, 3 z2, 4 u2; f/z2/u2 batch x h x w, z1/u1
+ * batch x n_coeff x h x w) into device memory in `dtype`. */
+typedef struct rk_admm_state rk_admm_state;
+int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0,
+                   double p1, const double* weights, int inner_cg_iterations, void* stream, rk_admm_state** admm);
+int rk_admm_iterate(rk_admm_state* admm, int64_t n, int64_t* failed_iteration, void* stream);
+int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* stream);
+int rk_admm_destroy(rk_admm_state* admm);
+
 /* ------------------------------------------------------------- instrumentation (no reference equivalent) */
 typedef enum {
   RK_KERNEL_PACK = 0,        /* layout packing (image / sinogram -> 4-image interleave) */

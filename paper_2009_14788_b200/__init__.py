@@ -21,6 +21,7 @@ from .rng import Rng
 from .solvers import cg, cgne, estimate_alpha, landweber
 from . import shearlet
 from .shearlet import ShearletPlan, backward, make_plan, make_plan_cached, shearlet_operator
+from .admm import AdmmParams, AdmmState, admm_objective, admm_reconstruct, default_weights, shrink
 
 
 def forward(plan_or_geometry, x, *args, **kwargs):
@@ -40,4 +41,5 @@ __all__ = [
     "filter_kind_name", "filter_sinogram", "make_filter", "LinearOperator", "adjoint_check", "compose",
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
     "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",
+    "AdmmParams", "AdmmState", "admm_objective", "admm_reconstruct", "default_weights", "shrink",
 ]

@@ -78,6 +78,11 @@ SIGNATURES = {
     "rk_shearlet_info": (_i, [_vp, _P(_i64), _vp, _vp]),
     "rk_shearlet_forward": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
     "rk_shearlet_backward": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
+    "rk_admm": (_i, [_vp, _vp, _i, _vp, _i64, _d, _d, _vp, _i64, _i, _vp, _P(_i64), _vp]),
+    "rk_admm_create": (_i, [_vp, _vp, _i, _vp, _i64, _d, _d, _vp, _i, _vp, _P(_vp)]),
+    "rk_admm_iterate": (_i, [_vp, _i64, _P(_i64), _vp]),
+    "rk_admm_read": (_i, [_vp, _i, _i, _vp, _vp]),
+    "rk_admm_destroy": (_i, [_vp]),
     "rk_profiling_enable": (_i, [_i]),
     "rk_profiling_read": (_i, [_vp, _i]),  # (rk_kernel_stats*, reset): pass ctypes.byref(RkKernelStats())
     "rk_probe_smem_bandwidth": (_i, [_i, _P(_d)]),

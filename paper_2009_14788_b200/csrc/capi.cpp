@@ -2,6 +2,7 @@
 // Each entry point validates like the reference function it replaces
 // (cited), enqueues the CUDA work and maps exceptions onto rk_status codes.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -522,6 +523,124 @@ int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int6
     RK_CUDA(cudaSetDevice(plan->s.device));
     rk::shearlet_backward(plan->s, dtype, d_coeff, batch, d_image, as_stream(stream));
   });
+}
+
+// ---------------------------------------------------------------- ADMM (admm.cpp:111-163)
+namespace {
+void check_admm_args(rk_plan* plan, rk_shearlet* sh, int dtype, int64_t batch, double p0, double p1) {
+  check_device_plan(plan);
+  require(sh != nullptr && sh->s.device >= 0, "shearlet plan is null or host-only");
+  require(sh->s.device == plan->p.device, "shearlet plan and projector plan live on different devices");
+  check_dtype(dtype);
+  require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
+  if (!(p0 > 0.0) || !(p1 > 0.0))
+    throw rk::ValidationError("admm penalties must be positive, got p0 = " + std::to_string(p0) +
+                              ", p1 = " + std::to_string(p1));
+  if (sh->s.height != plan->p.s || sh->s.width != plan->p.s)
+    throw rk::ValidationError("operator domain (" + std::to_string(plan->p.s) + ", " + std::to_string(plan->p.s) +
+                              ") does not match plan grid " + std::to_string(sh->s.height) + "x" +
+                              std::to_string(sh->s.width));
+}
+
+// default_weights (admm.cpp:11-15) or the caller's; thresh = scale(w, p0 / p1) (admm.cpp:135)
+std::vector<double> admm_thresholds(const rk::Shearlet& s, const double* weights, double p0, double p1) {
+  std::vector<double> t(static_cast<size_t>(s.n_coeff));
+  for (int64_t k = 0; k < s.n_coeff; ++k) {
+    const double w = weights ? weights[k] : std::pow(3.0, s.scales[size_t(k)]) / 400.0;
+    t[size_t(k)] = w * (p0 / p1);
+    if (!(t[size_t(k)] >= 0.0))
+      throw rk::ValidationError("shrink threshold must be nonnegative, got " + std::to_string(t[size_t(k)]) +
+                                " at index " + std::to_string(k));
+  }
+  return t;
+}
+}  // namespace
+
+struct rk_admm_state {
+  rk::Admm a;
+};
+
+int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0,
+                   double p1, const double* weights, int inner_cg_iterations, void* stream, rk_admm_state** out) {
+  return guarded([&] {
+    require(out != nullptr, "admm pointer is null");
+    *out = nullptr;
+    check_admm_args(plan, shearlet, dtype, batch, p0, p1);
+    require(d_sino != nullptr, "sinogram pointer is null");
+    if (inner_cg_iterations < 1) throw rk::ValidationError("admm inner_cg_iterations must be at least 1");
+    auto h = std::make_unique<rk_admm_state>();
+    rk::Admm& a = h->a;
+    a.plan = &plan->p;
+    a.sh = &shearlet->s;
+    a.dtype = dtype;
+    a.batch = batch;
+    a.p0f = float(p0);
+    a.p1f = float(p1);
+    a.sys = rk::CgSystem{float(p0), float(1.0 + p1)};
+    a.inner = inner_cg_iterations;
+    const std::vector<double> th = admm_thresholds(shearlet->s, weights, p0, p1);
+    ScratchLease lease(plan->p, as_stream(stream));
+    std::lock_guard<std::mutex> lock(shearlet->s.mu);
+    rk::admm_init(a, d_sino, th, as_stream(stream));
+    *out = h.release();
+  });
+}
+
+int rk_admm_iterate(rk_admm_state* admm, int64_t n, int64_t* failed_iteration, void* stream) {
+  return guarded([&] {
+    require(admm != nullptr, "admm is null");
+    if (n < 0) throw rk::ValidationError("admm outer_iterations must be nonnegative");
+    rk::Admm& a = admm->a;
+    int64_t failed = a.failed;
+    if (failed < 0 && n > 0) {
+      ScratchLease lease(*a.plan, as_stream(stream));
+      std::lock_guard<std::mutex> lock(a.sh->mu);
+      failed = rk::admm_iterate(a, n, as_stream(stream));
+    }
+    if (failed_iteration) *failed_iteration = failed;
+    if (failed >= 0)
+      throw rk::NumericalError("admm state became non-finite at iteration " + std::to_string(failed), int(failed));
+  });
+}
+
+int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* stream) {
+  return guarded([&] {
+    require(admm != nullptr, "admm is null");
+    require(d_dst != nullptr, "destination pointer is null");
+    check_dtype(dtype);
+    rk::Admm& a = admm->a;
+    RK_CUDA(cudaSetDevice(a.plan->device));
+    RK_CUDA(cudaStreamWaitEvent(as_stream(stream), a.plan->scratch_free, 0));
+    rk::admm_read(a, which, dtype, d_dst, as_stream(stream));
+  });
+}
+
+int rk_admm_destroy(rk_admm_state* admm) {
+  return guarded([&] {
+    if (!admm) return;
+    cudaSetDevice(admm->a.plan->device);
+    cudaDeviceSynchronize();
+    delete admm;
+  });
+}
+
+int rk_admm(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0, double p1,
+            const double* weights, int64_t outer_iterations, int inner_cg_iterations, void* d_image,
+            int64_t* failed_iteration, void* stream) {
+  rk_admm_state* h = nullptr;
+  int st = rk_admm_create(plan, shearlet, dtype, d_sino, batch, p0, p1, weights, inner_cg_iterations, stream, &h);
+  if (st != RK_OK) return st;
+  if (failed_iteration) *failed_iteration = -1;
+  st = rk_admm_iterate(h, outer_iterations, failed_iteration, stream);
+  if (st == RK_OK) st = rk_admm_read(h, 0, dtype, d_image, stream);
+  if (st == RK_OK) {
+    st = rk_admm_destroy(h);
+  } else {
+    const std::string err = rk_last_error();
+    rk_admm_destroy(h);
+    g_last_error = err;  // keep the first failure's message
+  }
+  return st;
 }
 
 int rk_profiling_enable(int enable) {

@@ -457,6 +457,14 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
       // narrowed through the storage precision like a user-visible result
       *dst = make_float4(float(from_f32<TOut>(acc[r].x)), float(from_f32<TOut>(acc[r].y)),
                          float(from_f32<TOut>(acc[r].z)), float(from_f32<TOut>(acc[r].w)));
+    } else if (epi.mode == kOutSystem) {
+      // axpy(p0, A'A x, scale(x, 1 + p1)) in fp32 (admm.cpp:142, tensor.cpp:334-347)
+      const float4 x = __ldg(epi.src + (dst - epi.packed));
+      const float c0 = epi.c0, c1 = epi.c1;
+      *dst = make_float4(__fadd_rn(__fmul_rn(c0, acc[r].x), __fmul_rn(c1, x.x)),
+                         __fadd_rn(__fmul_rn(c0, acc[r].y), __fmul_rn(c1, x.y)),
+                         __fadd_rn(__fmul_rn(c0, acc[r].z), __fmul_rn(c1, x.z)),
+                         __fadd_rn(__fmul_rn(c0, acc[r].w), __fmul_rn(c1, x.w)));
     } else {
       // Landweber update x <- (-alpha) * grad + x in fp32 (solvers.cpp:139, tensor.cpp:338-343)
       const float4 x = *dst;

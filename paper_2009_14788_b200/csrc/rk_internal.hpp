@@ -161,6 +161,50 @@ void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1
 void shearlet_admm_synth(Shearlet& sp, const float* z1, const float* u1, int64_t batch, float* image,
                          cudaStream_t st);
 
+// CG system coefficients: (c0 A'A + c1 I) (solver.cu cg_packed)
+struct CgSystem {
+  float c0, c1;
+};
+
+// l1-shearlet ADMM state (admm.cu; reference admm.cpp:111-163).  Radon-side
+// vectors in the packed image layout, shearlet-side split/dual variables in the
+// coefficient layout [B][K][n][n]; fp32 throughout (the reference's float path).
+struct Admm {
+  Plan* plan = nullptr;
+  Shearlet* sh = nullptr;
+  int dtype = 1;
+  int64_t batch = 0;
+  CgSystem sys{0.f, 0.f};
+  float p0f = 0.f, p1f = 0.f;
+  int inner = 0;
+  int64_t iterations_done = 0;
+  int failed = -1;  // first outer iteration whose state turned non-finite
+  DeviceBuffer packed;   // F, BP, Z2, U2, CGY, 4 CG work planes
+  DeviceBuffer sino;     // packed sinogram scratch
+  DeviceBuffer user;     // fU, shU  ([B][n][n] fp32)
+  DeviceBuffer coeff;    // z1, u1   ([B][K][n][n] fp32)
+  DeviceBuffer small;    // thresholds, flags, CG scalars
+  float4* F = nullptr;
+  float4* BP = nullptr;
+  float4* Z2 = nullptr;
+  float4* U2 = nullptr;
+  float4* CGY = nullptr;
+  float4* work = nullptr;
+  float* fU = nullptr;
+  float* shU = nullptr;
+  float* z1 = nullptr;
+  float* u1 = nullptr;
+  float* thresh = nullptr;
+  int* flags = nullptr;  // [0] divergence iteration, [1] CG non-positive curvature
+  void* cg_scalars = nullptr;
+};
+// bp = A'y, zero state; thresholds[k] = w_k p0 / p1 in fp64, used as float (admm.cpp:129-140)
+void admm_init(Admm& a, const void* d_sino, const std::vector<double>& thresholds, cudaStream_t st);
+// n outer iterations (admm.cpp:146-160); returns the first failed iteration or -1
+int64_t admm_iterate(Admm& a, int64_t n, cudaStream_t st);
+// which: 0 f, 1 z1, 2 u1, 3 z2, 4 u2 -> dst in the storage dtype
+void admm_read(Admm& a, int which, int dtype, void* dst, cudaStream_t st);
+
 // ----------------------------------------------------------------- host helpers (plan.cpp)
 rk_geometry resolve_geometry(const rk_geometry& in);
 void build_plan(Plan& p);
@@ -177,7 +221,8 @@ void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int
 // reference-shaped result); kOutPacked: packed float4 layout (values narrowed
 // through the dtype first); forward kOutResidual: packed (A x - y); backprojection
 // kOutAxpy: packed x <- (-alpha) * (A' r) + x with a non-finite flag.
-enum { kOutUser = 0, kOutPacked = 1, kOutResidual = 2, kOutAxpy = 3 };
+// kOutSystem: packed out = c0 * (A' s) + c1 * src (the ADMM CG system, admm.cpp:142).
+enum { kOutUser = 0, kOutPacked = 1, kOutResidual = 2, kOutAxpy = 3, kOutSystem = 4 };
 struct FwdEpilogue {
   int mode = kOutUser;
   float4* packed = nullptr;       // [G][na][nd]
@@ -189,6 +234,8 @@ struct BpEpilogue {
   float neg_alpha = 0.f;     // kOutAxpy
   int* flag = nullptr;       // kOutAxpy: atomicMin(iteration) on a non-finite iterate
   int iteration = 0;
+  const float4* src = nullptr;  // kOutSystem
+  float c0 = 0.f, c1 = 0.f;
 };
 
 // packed image -> its transpose ([G][s+2][s+2], rows <-> columns)
@@ -210,6 +257,11 @@ void unpack_images(int dtype, const float4* src, int64_t batch, int64_t s, void*
 // return the first failing iteration (DivergenceError / NotPositiveDefiniteError) or -1
 int run_landweber(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, double alpha,
                   int iterations, void* d_x, cudaStream_t st);
+// CG over packed images (solver.cu; solvers.cpp:47-107) on A'A x = b (sys null) or
+// (c0 A'A + c1 I) x = b; x updated in place; work = 4 packed image planes.
+size_t cg_scalar_bytes(int64_t batch);
+void cg_packed(Plan& p, int64_t batch, const float4* b, float4* x, int max_iter, double tol, const CgSystem* sys,
+               float4* work, float4* sino, void* scalars, int* npd, cudaStream_t st);
 int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter, double tol,
              void* d_x, cudaStream_t st);
 double run_estimate_alpha(Plan& p, int iterations, uint64_t seed, cudaStream_t st);

@@ -300,29 +300,42 @@ int run_landweber(Plan& p, int dtype, const void* d_y, const void* d_guess, int6
   return h_flag == none ? -1 : h_flag;
 }
 
-// solvers.cpp:47-107 + 162-166 (CG on A'A x = A'y)
-int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter, double tol,
-             void* d_x, cudaStream_t st) {
-  if (max_iter < 0) throw ValidationError("cg max_iter must be >= 0");
-  if (tol < 0.0) throw ValidationError("cg tolerance must be >= 0");
-  const int64_t G = groups_of(batch), P = p.s + 2;
-  const int64_t img_plane = P * P, sino_plane = p.na * p.nd;
-  const size_t ib = size_t(G * img_plane) * sizeof(float4), sb = size_t(G * sino_plane) * sizeof(float4);
-  // x, r, p, ap, b, transposed scratch | sinogram scratch
-  p.solver_a.reserve(6 * ib);
-  p.solver_c.reserve(sb);
+size_t cg_scalar_bytes(int64_t batch) {
+  const size_t ne = size_t(groups_of(batch) * kPack);
+  return size_t(groups_of(batch)) * kRedBlocks * sizeof(double4) + ne * (4 * sizeof(double) + 2 * sizeof(float) + 4 * sizeof(int)) + 64;
+}
+
+// system apply over packed images: out = A'(A in)  (sys == nullptr, solvers.cpp:164)
+// or out = c0 A'(A in) + c1 in  (admm.cpp:142: axpy(p0, A'A x, scale(x, 1 + p1)))
+static void apply_system(Plan& p, const float4* in, float4* out, int64_t batch, const CgSystem* sys, float4* xt,
+                         float4* sino, cudaStream_t st) {
+  FwdEpilogue fe;
+  fe.mode = kOutPacked;
+  fe.packed = sino;
+  apply_forward(p, in, xt, batch, fe, st);
+  BpEpilogue be;
+  be.mode = sys ? kOutSystem : kOutPacked;
+  be.packed = out;
+  if (sys) {
+    be.src = in;
+    be.c0 = sys->c0;
+    be.c1 = sys->c1;
+  }
+  launch_backproject(p, sino, batch, RK_F32, nullptr, st, be);
+}
+
+// solvers.cpp:47-107: CG from x (updated in place) on the packed system; the
+// image borders of b and x are zero.  work: 4 packed image planes (r, p, ap,
+// transposed scratch); npd receives atomicMin(first non-positive-curvature iteration).
+void cg_packed(Plan& p, int64_t batch, const float4* Bv, float4* X, int max_iter, double tol, const CgSystem* sys,
+               float4* work, float4* S, void* scalars, int* npd, cudaStream_t st) {
+  const int64_t G = groups_of(batch), P = p.s + 2, img_plane = P * P;
   const size_t ne = size_t(G * kPack);
-  p.solver_scalars.reserve(ne * (4 * sizeof(double) + 2 * sizeof(float) + 4 * sizeof(int)) + 64 +
-                           size_t(G) * kRedBlocks * sizeof(double4));
-  char* base = p.solver_a.as<char>();
-  float4* X = reinterpret_cast<float4*>(base);
-  float4* R = reinterpret_cast<float4*>(base + ib);
-  float4* Pv = reinterpret_cast<float4*>(base + 2 * ib);
-  float4* AP = reinterpret_cast<float4*>(base + 3 * ib);
-  float4* Bv = reinterpret_cast<float4*>(base + 4 * ib);
-  float4* T = reinterpret_cast<float4*>(base + 5 * ib);
-  float4* S = p.solver_c.as<float4>();
-  char* sc = p.solver_scalars.as<char>();
+  float4* R = work;
+  float4* Pv = work + G * img_plane;
+  float4* AP = work + 2 * G * img_plane;
+  float4* T = work + 3 * G * img_plane;
+  char* sc = static_cast<char*>(scalars);
   double4* partial = reinterpret_cast<double4*>(sc);
   sc += size_t(G) * kRedBlocks * sizeof(double4);
   CgScalars c;
@@ -335,43 +348,26 @@ int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t b
   c.done = reinterpret_cast<int*>(c.beta + ne);
   c.act = c.done + ne;
   c.pupd = c.act + ne;
-  c.npd = c.pupd + ne;
-  const int none = INT_MAX;
-  RK_CUDA(cudaMemcpyAsync(c.npd, &none, sizeof(int), cudaMemcpyHostToDevice, st));
-
-  // b = A'y, narrowed to the storage precision like op.adjoint(y) (solvers.cpp:163)
-  launch_pack_sino(dtype, d_y, batch, p.na, p.nd, S, st);
-  BpEpilogue pk;
-  pk.mode = kOutPacked;
-  pk.packed = Bv;
-  RK_CUDA(cudaMemsetAsync(Bv, 0, ib, st));
-  launch_backproject(p, S, batch, dtype, nullptr, st, pk);
-  // x = guess; r = b - A'A x; p = r
-  launch_pack_images(dtype, d_guess, batch, p.s, X, st);
-  FwdEpilogue fe;
-  fe.mode = kOutPacked;
-  fe.packed = S;
-  BpEpilogue be;
-  be.mode = kOutPacked;
-  be.packed = AP;
-  RK_CUDA(cudaMemsetAsync(AP, 0, ib, st));
-  apply_forward(p, X, T, batch, fe, st);
-  launch_backproject(p, S, batch, RK_F32, nullptr, st, be);
+  c.npd = npd;
+  // the backprojection writes interiors only: keep ap's border zero
+  RK_CUDA(cudaMemsetAsync(AP, 0, size_t(G * img_plane) * sizeof(float4), st));
+  // r = b - apply(x); p = r (solvers.cpp:51-52)
+  apply_system(p, X, AP, batch, sys, T, S, st);
   {
     KernelTimer t(RK_KERNEL_SOLVER, st);
     sub_kernel<<<grid_for(G * img_plane, 256), 256, 0, st>>>(Bv, AP, G * img_plane, R);
   }
-  RK_CUDA(cudaMemcpyAsync(Pv, R, ib, cudaMemcpyDeviceToDevice, st));
+  RK_CUDA(cudaMemcpyAsync(Pv, R, size_t(G * img_plane) * sizeof(float4), cudaMemcpyDeviceToDevice, st));
   dot(R, R, G, img_plane, partial, c.rs, st);
   dot(Bv, Bv, G, img_plane, partial, c.normb, st);
   {
     KernelTimer t(RK_KERNEL_SOLVER, st);
     cg_init_kernel<<<grid_for(batch, 128), 128, 0, st>>>(c, batch, tol);
   }
-  RK_CUDA(cudaMemsetAsync(c.done + batch, 0xff, sizeof(int) * (ne - size_t(batch)), st));  // padding: frozen
+  if (ne > size_t(batch))
+    RK_CUDA(cudaMemsetAsync(c.done + batch, 0xff, sizeof(int) * (ne - size_t(batch)), st));  // padding: frozen
   for (int it = 0; it < max_iter; ++it) {
-    apply_forward(p, Pv, T, batch, fe, st);
-    launch_backproject(p, S, batch, RK_F32, nullptr, st, be);
+    apply_system(p, Pv, AP, batch, sys, T, S, st);
     dot(Pv, AP, G, img_plane, partial, c.pap, st);
     {
       KernelTimer t(RK_KERNEL_SOLVER, st);
@@ -394,9 +390,43 @@ int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t b
       cg_p_kernel<<<dim3(grid_for(img_plane, 256, 512), unsigned(G)), 256, 0, st>>>(Pv, R, img_plane, c);
     }
   }
+}
+
+// solvers.cpp:47-107 + 162-166 (CG on A'A x = A'y)
+int run_cgne(Plan& p, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter, double tol,
+             void* d_x, cudaStream_t st) {
+  if (max_iter < 0) throw ValidationError("cg max_iter must be >= 0");
+  if (tol < 0.0) throw ValidationError("cg tolerance must be >= 0");
+  const int64_t G = groups_of(batch), P = p.s + 2;
+  const int64_t img_plane = P * P, sino_plane = p.na * p.nd;
+  const size_t ib = size_t(G * img_plane) * sizeof(float4), sb = size_t(G * sino_plane) * sizeof(float4);
+  // x, b, 4 CG work planes | sinogram scratch
+  p.solver_a.reserve(6 * ib);
+  p.solver_c.reserve(sb);
+  p.solver_scalars.reserve(cg_scalar_bytes(batch) + 64);
+  char* base = p.solver_a.as<char>();
+  float4* X = reinterpret_cast<float4*>(base);
+  float4* Bv = reinterpret_cast<float4*>(base + ib);
+  float4* work = reinterpret_cast<float4*>(base + 2 * ib);
+  float4* S = p.solver_c.as<float4>();
+  int* npd = p.solver_scalars.as<int>();
+  void* scalars = p.solver_scalars.as<char>() + 64;
+  const int none = INT_MAX;
+  RK_CUDA(cudaMemcpyAsync(npd, &none, sizeof(int), cudaMemcpyHostToDevice, st));
+
+  // b = A'y, narrowed to the storage precision like op.adjoint(y) (solvers.cpp:163)
+  launch_pack_sino(dtype, d_y, batch, p.na, p.nd, S, st);
+  BpEpilogue pk;
+  pk.mode = kOutPacked;
+  pk.packed = Bv;
+  RK_CUDA(cudaMemsetAsync(Bv, 0, ib, st));
+  launch_backproject(p, S, batch, dtype, nullptr, st, pk);
+  // x = guess
+  launch_pack_images(dtype, d_guess, batch, p.s, X, st);
+  cg_packed(p, batch, Bv, X, max_iter, tol, nullptr, work, S, scalars, npd, st);
   unpack_images(dtype, X, batch, p.s, d_x, st);
   int h_npd = none;
-  RK_CUDA(cudaMemcpyAsync(&h_npd, c.npd, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaMemcpyAsync(&h_npd, npd, sizeof(int), cudaMemcpyDeviceToHost, st));
   RK_CUDA(cudaStreamSynchronize(st));
   return h_npd == none ? -1 : h_npd;
 }
