@@ -1,6 +1,7 @@
 """Command-line front end for the hot path — the subcommands of the reference
 CLI that reach it (``proj/tools/cli.cpp``): ``project``, ``backproject``,
-``filter``, ``fbp``, ``solve``, ``check-adjoint`` and ``bench``, with the same
+``filter``, ``fbp``, ``solve``, ``check-adjoint``, ``bench``, ``phantom``,
+``shearlet`` and ``admm``, with the same
 flags (angles in degrees, geometry defaults, ``--precision``), ``.npy`` files
 holding the natural rank (a batch dim is lifted/squeezed like
 ``lift_batch``/``squeeze_batch``, cli.cpp:109-129), the same ``--json``
@@ -25,10 +26,14 @@ VERSION = "radon_b200 0.1"
 
 
 def _geo_args(p, admm_names=False):
+    """cli.cpp:50-74; admm_names swaps in the --n-angles / --angles-range spellings."""
     p.add_argument("--geometry", default="parallel", choices=["parallel", "fanbeam"])
-    p.add_argument("--angles", type=int, default=0, help="projection angle count (default: from input / size)")
-    p.add_argument("--angle-start", type=float, default=math.nan, help="first angle in degrees (default 0)")
-    p.add_argument("--angle-range", type=float, default=math.nan, help="span in degrees (180 parallel, 360 fan)")
+    p.add_argument("--n-angles" if admm_names else "--angles", dest="angles", type=int, default=0,
+                   help="projection angle count (default: from input / size)")
+    p.add_argument("--angle-start", type=float, default=math.nan,
+                   help="first angle in degrees (default " + ("-range/2)" if admm_names else "0)"))
+    p.add_argument("--angles-range" if admm_names else "--angle-range", dest="angle_range", type=float,
+                   default=math.nan, help="span in degrees (180 parallel, 360 fan)")
     p.add_argument("--det-count", type=int, default=0)
     p.add_argument("--det-spacing", type=float, default=0.0)
     p.add_argument("--source-distance", type=float, default=0.0, help="fan-beam (default: image size)")
@@ -36,14 +41,15 @@ def _geo_args(p, admm_names=False):
     p.add_argument("--step", type=float, default=1.0)
 
 
-def build_geometry(a, image_size, n_angles):
-    """cli.cpp:76-97 (degrees -> radians through angles_linspace)."""
+def build_geometry(a, image_size, n_angles, centered=False):
+    """cli.cpp:76-97 (degrees -> radians through angles_linspace); centered: the
+    default start is -range/2 (admm)."""
     import paper_2009_14788_b200 as rk
 
     if n_angles < 1:
         raise ValidationError(f"angle count must be >= 1, got {n_angles}")
     rng = a.angle_range if not math.isnan(a.angle_range) else (360.0 if a.geometry == "fanbeam" else 180.0)
-    start = a.angle_start if not math.isnan(a.angle_start) else 0.0
+    start = a.angle_start if not math.isnan(a.angle_start) else (-rng / 2.0 if centered else 0.0)
     ang = [d * (math.pi / 180.0) for d in rk.angles_linspace(start, start + rng, n_angles)]
     dc = a.det_count if a.det_count > 0 else None
     ds = a.det_spacing if a.det_spacing > 0 else None
@@ -165,6 +171,31 @@ def main(argv=None) -> int:
     p.add_argument("--precision", choices=list(_PREC), default="single")
     p.add_argument("--warmup", type=int, default=1)
     p.add_argument("--runs", type=int, default=5)
+    p = sub.add_parser("phantom", help="write a Shepp-Logan head phantom")
+    p.add_argument("--size", type=int, default=512)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--precision", choices=list(_PREC), default="single")
+    p = sub.add_parser("shearlet", help="alpha-shearlet analysis or synthesis")
+    p.add_argument("--in", dest="inp", required=True, help="input .npy (image, or coefficients with --inverse)")
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--scales", type=int, default=5)
+    p.add_argument("--alpha", type=float, default=0.5)
+    p.add_argument("--inverse", action="store_true", help="synthesize an image from coefficients")
+    p.add_argument("--cache-dir", default="", help="plan cache directory (default: RADONKIT_CACHE_DIR)")
+    p = sub.add_parser("admm", help="l1-shearlet regularized reconstruction")
+    _geo_args(p, admm_names=True)
+    p.add_argument("--size", type=int, required=True)
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("-o", "--out", required=True)
+    p.add_argument("--scales", type=int, default=5)
+    p.add_argument("--alpha", type=float, default=0.5)
+    p.add_argument("--p0", type=float, default=0.02)
+    p.add_argument("--p1", type=float, default=0.1)
+    p.add_argument("--outer", type=int, default=50)
+    p.add_argument("--inner", type=int, default=50)
+    p.add_argument("--progress", action="store_true", help="print the objective each outer iteration to stderr")
+    p.add_argument("--cache-dir", default="")
+    p.add_argument("--reference", default="")
     a = ap.parse_args(argv)
     try:
         return _run(rk, a)
@@ -295,7 +326,74 @@ def _run(rk, a) -> int:
             print(f"{VERSION}\nforward: {fwd['median_ms']:.3f} ms/call median, {fwd['images_per_s']:.2f} images/s")
             print(f"backprojection: {bwd['median_ms']:.3f} ms/call median, {bwd['images_per_s']:.2f} images/s")
         return 0
+    if a.cmd == "phantom":  # cli.cpp:243-251
+        from .phantom import shepp_logan
+
+        _write(a.out, shepp_logan(a.size, _PREC[a.precision]))
+        return 0
+    if a.cmd == "shearlet":  # cli.cpp:440-476
+        if a.scales < 1:
+            raise ValidationError("--scales must be positive")
+        alphas = [a.alpha] * a.scales
+        x = np.load(a.inp)
+        if a.inverse:
+            co = _lift(x, 4)
+            plan = rk.make_plan_cached(co.shape[2], co.shape[3], alphas, a.cache_dir)
+            if plan.n_coeff != co.shape[1]:
+                raise ValidationError(f"coefficient count {co.shape[1]} does not match the plan's {plan.n_coeff}")
+            _write(a.out, _host(rk.backward(plan, _to_dev(co))))
+        else:
+            img = _lift(x, 3)
+            plan = rk.make_plan_cached(img.shape[1], img.shape[2], alphas, a.cache_dir)
+            _write(a.out, _host(rk.forward(plan, _to_dev(img))))
+        return 0
+    if a.cmd == "admm":  # cli.cpp:478-556
+        if a.scales < 1 or not (a.p0 > 0) or not (a.p1 > 0) or a.outer < 0 or a.inner < 1:
+            raise ValidationError("--scales, --p0, --p1, --inner must be positive and --outer nonnegative")
+        sino = _read(a.inp, 3)
+        if a.det_count == 0:
+            a.det_count = sino.shape[2]
+        g = build_geometry(a, a.size, a.angles if a.angles > 0 else sino.shape[1], centered=True)
+        op = rk.projector_operator(g, rk.ProjectorOptions(a.step))
+        plan = rk.make_plan_cached(a.size, a.size, [a.alpha] * a.scales, a.cache_dir)
+        y = _to_dev(sino)
+        prm = rk.AdmmParams(p0=a.p0, p1=a.p1, outer_iterations=a.outer, inner_cg_iterations=a.inner)
+        obs = None
+        if a.progress:
+            def obs(it, st):
+                print(f"iter {it} objective {rk.admm_objective(op, plan, st.f, y):.6e}", file=sys.stderr)
+        t0 = time.perf_counter()
+        x = rk.admm_reconstruct(op, plan, y, prm, obs)
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        rec = _host(x)
+        _write(a.out, rec)
+        objective = rk.admm_objective(op, plan, x, y)
+        rep = {"command": "admm", "outer": a.outer, "inner": a.inner, "p0": a.p0, "p1": a.p1, "scales": a.scales,
+               "alpha": a.alpha, "seconds": secs, "objective": objective, "geometry": geometry_json(g),
+               "output": a.out}
+        if a.reference:
+            ref = np.load(a.reference).astype(np.float64)
+            rep["mse_vs_reference"] = float(np.mean((rec.reshape(ref.shape).astype(np.float64) - ref) ** 2))
+        if a.json:
+            print(json.dumps(rep, indent=2))
+        else:
+            print(f"admm: {a.outer} outer x {a.inner} inner iterations, objective {objective:.6e}, {secs:.3f} s")
+            if a.reference:
+                print(f"mse vs reference: {rep['mse_vs_reference']:.6e}")
+        return 0
     return 1
+
+
+def _lift(x, want):
+    """lift_batch (cli.cpp:109-122)."""
+    if x.ndim == want - 1:
+        return x[None]
+    if x.ndim != want:
+        raise ValidationError(f"expected a {want - 1}-d or batched {want}-d array, got shape {x.shape}")
+    if x.dtype not in (np.float16, np.float32, np.float64):
+        raise ValidationError(f"unsupported dtype {x.dtype}")
+    return x
 
 
 if __name__ == "__main__":

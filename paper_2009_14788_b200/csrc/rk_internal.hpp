@@ -142,9 +142,11 @@ struct Shearlet {
   int64_t height = 0, width = 0, n_coeff = 0;
   std::vector<double> alphas, scales;
   std::vector<double> multipliers;  // n_coeff x h x w (fp64, natural layout)
-  DeviceBuffer d_mult_t;            // fp32, per coefficient transposed (column-major) grid
-  DeviceBuffer d_twiddle;           // float2, h/2 forward twiddles
-  DeviceBuffer d_mult_t64, d_twiddle64;  // fp64 copies for fp64 storage (built on first use)
+  // device tables (shearlet.cu): coefficient pairs {M_2j, M_2j+1} per bin in
+  // bit-reversed row and column order (the order the DIF passes leave spectra
+  // in), and the n/2 forward twiddles; fp32 built with the plan, fp64 on first use
+  DeviceBuffer d_mult2, d_twiddle;
+  DeviceBuffer d_mult2_64, d_twiddle64;
   DeviceBuffer work_a, work_b;      // spectra scratch
   std::mutex mu;
 };

@@ -1,18 +1,27 @@
 // Alpha-shearlet analysis / synthesis on the device (§8f rank 3; reference
 // shearlet.cpp:253-330): coefficient k of an image x is
-// Re(ifft2(fft2(x) * M_k)); synthesis sums fft2(c_k) * M_k over k in
-// ascending order and takes Re(ifft2(.)).  Arithmetic follows the reference's
-// precision split (shearlet.cpp:303-310): fp64 storage computes in fp64
-// (spec_d), fp32 / fp16 storage in fp32 (spec_f); power-of-two grids.
+// Re(ifft2(fft2(x) * M_k)); synthesis sums fft2(c_k) * M_k over k and takes
+// Re(ifft2(.)).  Arithmetic follows the reference's precision split
+// (shearlet.cpp:303-310): fp64 storage computes in fp64, fp32 / fp16 storage
+// in fp32; power-of-two grids.
 //
-// 2-D FFT = row FFTs, a tiled transpose, row FFTs: the spectra are kept in
-// the transposed layout Xt[b][col][row] so every pass is a row pass of a
-// shared-memory radix-2 FFT, and the multipliers are pre-transposed on the
-// host.  The multiply, the inverse transform's conjugations, the 1/(h w)
-// normalisation, the real-part extraction and the synthesis accumulation are
-// fused into the load / store of the row passes.  Analysis walks the
-// (image, coefficient) planes in chunks small enough that a chunk's two
-// complex scratch planes stay resident in L2 between passes.
+// Layout and passes (no transposes, no bit-reversal permutes):
+//   * 2-D FFTs are a row pass and a column pass over natural [row][col]
+//     planes, each a shared-memory radix-2 FFT of a CTA tile (rows, or a
+//     tile of adjacent columns read with coalesced row segments).
+//   * Forward transforms are decimation-in-frequency (natural in, bit-reversed
+//     out) and inverse ones decimation-in-time (bit-reversed in, natural out),
+//     so spectra live in bit-reversed (row, col) order and the multipliers are
+//     stored in that order on the host side of the plan.
+//   * Two coefficients share one complex transform.  Analysis: M_k and
+//     M_k+1 are real and even, so ifft2(X (M_k + i M_k+1)) = c_k + i c_k+1
+//     (both real).  Synthesis: with Z = fft2(c_k + i c_k+1),
+//     Z (M_k - i M_k+1) = [C_k M_k + C_k+1 M_k+1] + i[C_k+1 M_k - C_k M_k+1]
+//     whose second term is anti-Hermitian, so Re(ifft2(sum)) is exactly the
+//     synthesis.  This halves the FFT work and the intermediate traffic.
+//   * Analysis walks (coefficient pair, image) items pair-major so one pair's
+//     multipliers stay in L2 across the batch; synthesis accumulates a fixed
+//     chunk of pairs per column tile in registers (a batch-independent order).
 //
 // ADMM hooks (admm.cu, admm.cpp:146-156): analysis can fuse the shrink and
 // dual update into its store (z1 = shrink(c + u1, t_k), u1 += c - z1, with a
@@ -24,8 +33,6 @@
 namespace rk {
 
 namespace {
-
-constexpr int kFftThreads = 256;
 
 template <class R>
 struct Cx;
@@ -59,103 +66,54 @@ template <class C>
 __device__ __forceinline__ C cmul(C a, C b) {
   return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
 }
-
-// R rows of n complex values in shared memory (bit-reversed order on entry) ->
-// forward DFT of each row (natural order).
 template <class C>
-__device__ void fft_rows_smem(C* a, int rows, int n, const C* __restrict__ tw) {
-  const int halfn = n >> 1;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-  for (int len = 2; len <= n; len <<= 1) {
-    const int half = len >> 1, stride = n / len;
-    for (int b = tid; b < rows * halfn; b += nt) {
-      const int r = b / halfn, bb = b - r * halfn;
-      const int grp = bb / half, k = bb - grp * half;
-      C* row = a + r * n;
-      const int i = grp * len + k;
-      const C u = row[i], v = cmul(row[i + half], tw[k * stride]);
+__device__ __forceinline__ C cmul_conj(C a, C b) {  // a * conj(b)
+  return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+}
+
+constexpr int kTileMin = 4096;  // complex elements per CTA tile (>= one row, <= one plane)
+constexpr int kPerThread = 16;  // tile elements per thread
+constexpr int kPairChunk = 8;   // coefficient pairs per synthesis accumulation (fixed: batch-independent order)
+
+// tile elements for an n x n plane: kTileMin, at least one row, at most the plane
+__host__ __device__ inline int tile_of(int n) { return min(max(kTileMin, n), n * n); }
+
+// cnt sequences of n = 2^logn complex values at stride ld.  DIF forward:
+// natural in, bit-reversed out, W = exp(-2 pi i / n).
+template <class C>
+__device__ void fft_dif(C* a, int cnt, int logn, int ld, const C* __restrict__ tw) {
+  const int halfn = 1 << (logn - 1);
+  const int tid = threadIdx.x, nt = blockDim.x, total = cnt * halfn;
+  for (int s = logn; s >= 1; --s) {
+    const int half = 1 << (s - 1), tsh = logn - s;
+    for (int b = tid; b < total; b += nt) {
+      const int r = b >> (logn - 1), bb = b & (halfn - 1);
+      const int k = bb & (half - 1), i = ((bb >> (s - 1)) << s) + k;
+      C* row = a + r * ld;
+      const C u = row[i], v = row[i + half];
       row[i] = {u.x + v.x, u.y + v.y};
-      row[i + half] = {u.x - v.x, u.y - v.y};
+      row[i + half] = cmul(C{u.x - v.x, u.y - v.y}, tw[k << tsh]);
     }
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ int brev(int k, int logn) { return int(__brev(unsigned(k)) >> (32 - logn)); }
-
-// forward FFT of real rows: out[r] = fft(in[r] (- sub[r])); rows are contiguous
-// in planes of rpp rows, plane p of the source at p * pstride
-template <class T, class R>
-__global__ void __launch_bounds__(kFftThreads)
-    rowfft_real_kernel(const T* __restrict__ in, const T* __restrict__ sub, int64_t pstride, int64_t rows, int n,
-                       int logn, const typename Cx<R>::T* __restrict__ tw, typename Cx<R>::T* __restrict__ out) {
-  using C = typename Cx<R>::T;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C* sm = reinterpret_cast<C*>(smraw);
-  const int nr = int(min(int64_t(blockDim.y), rows - int64_t(blockIdx.x) * blockDim.y));
-  const int64_t r0 = int64_t(blockIdx.x) * blockDim.y;
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y) {
-    const int r = e / n, c = e - r * n;
-    const int64_t rr = r0 + r, p = rr / n, lr = rr - p * n;
-    const int64_t off = p * pstride + lr * n + c;
-    R v = ld_r<R>(in + off);
-    if (sub) v = v - ld_r<R>(sub + off);  // sub(z1, u1) (admm.cpp:147)
-    sm[r * n + brev(c, logn)] = {v, R(0)};
-  }
-  __syncthreads();
-  fft_rows_smem(sm, nr, n, tw);
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y)
-    out[(r0 + e / n) * n + (e % n)] = sm[e];
-}
-
-// Complex row pass over planes of n rows.
-// mode 0: forward, out = fft(in)                        in plane = p
-// mode 1: inverse with multiplier, out = conj(fft(conj(in * m)))  (= n ifft(in m));
-//         plane p of the chunk is (image, coeff) q = q0 + p: in plane q / K, m plane q % K
-// mode 2: forward + accumulate, out += fft(in) * m      in plane = p, m plane = q0
-// mode 3: inverse, out = conj(fft(conj(in)))            in plane = p
-template <class R>
-__global__ void __launch_bounds__(kFftThreads)
-    rowfft_c2c_kernel(const typename Cx<R>::T* __restrict__ in, int64_t rows, int n, int logn,
-                      const typename Cx<R>::T* __restrict__ tw, int mode, const R* __restrict__ mult, int64_t q0,
-                      int64_t K, typename Cx<R>::T* __restrict__ out) {
-  using C = typename Cx<R>::T;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C* sm = reinterpret_cast<C*>(smraw);
-  const int nr = int(min(int64_t(blockDim.y), rows - int64_t(blockIdx.x) * blockDim.y));
-  const int64_t r0 = int64_t(blockIdx.x) * blockDim.y;
-  const int64_t plane = int64_t(n) * n;
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y) {
-    const int r = e / n, c = e - r * n;
-    const int64_t rr = r0 + r, p = rr / n, lr = rr - p * n;
-    C v;
-    if (mode == 1) {
-      const int64_t q = q0 + p;
-      v = in[(q / K) * plane + lr * n + c];
-      const R m = mult[(q % K) * plane + lr * n + c];
-      v = {v.x * m, -(v.y * m)};
-    } else {
-      v = in[rr * n + c];
-      if (mode == 3) v.y = -v.y;
+// DIT inverse (unnormalised): bit-reversed in, natural out, W = exp(+2 pi i / n).
+template <class C>
+__device__ void ifft_dit(C* a, int cnt, int logn, int ld, const C* __restrict__ tw) {
+  const int halfn = 1 << (logn - 1);
+  const int tid = threadIdx.x, nt = blockDim.x, total = cnt * halfn;
+  for (int s = 1; s <= logn; ++s) {
+    const int half = 1 << (s - 1), tsh = logn - s;
+    for (int b = tid; b < total; b += nt) {
+      const int r = b >> (logn - 1), bb = b & (halfn - 1);
+      const int k = bb & (half - 1), i = ((bb >> (s - 1)) << s) + k;
+      C* row = a + r * ld;
+      const C u = row[i], v = cmul_conj(row[i + half], tw[k << tsh]);
+      row[i] = {u.x + v.x, u.y + v.y};
+      row[i + half] = {u.x - v.x, u.y - v.y};
     }
-    sm[r * n + brev(c, logn)] = v;
-  }
-  __syncthreads();
-  fft_rows_smem(sm, nr, n, tw);
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y) {
-    const int r = e / n, c = e - r * n;
-    const int64_t rr = r0 + r;
-    const C v = sm[e];
-    if (mode == 1 || mode == 3) {
-      out[rr * n + c] = {v.x, -v.y};
-    } else if (mode == 2) {
-      const int64_t lr = rr % n;
-      const R m = mult[q0 * plane + lr * n + c];
-      const C a = out[rr * n + c];
-      out[rr * n + c] = {a.x + v.x * m, a.y + v.y * m};
-    } else {
-      out[rr * n + c] = v;
-    }
+    __syncthreads();
   }
 }
 
@@ -175,77 +133,247 @@ __device__ __forceinline__ float soft(float a, float b) {
   return a < 0.f ? -m : (a > 0.f ? m : 0.f);
 }
 
-// inverse row pass with real output: Re(conj(fft(conj(in)))) * scale stored
-// contiguously at out + (row r0 + r) * n (+ the ADMM update when requested)
+__device__ __forceinline__ void admm_update(const AdmmStore& a, int64_t gi, int k, float c) {
+  const float u = a.u1[gi];
+  const float z = soft(__fadd_rn(c, u), a.thresh[k]);
+  const float un = __fadd_rn(u, __fsub_rn(c, z));
+  a.z1[gi] = z;
+  a.u1[gi] = un;
+  if (!isfinite(un)) atomicMin(a.flag, a.iteration);
+}
+
+// ---------------------------------------------------------------- row passes
+// A CTA owns `nr` consecutive rows of one plane (nr * n = tile elements).
+
+// forward row DIF of real input rows: out[p] = rowDIF(in0[p] (- sub0[p]) + i (in1[p] (- sub1[p])))
+// plane p -> sources by `map`:
+//   map 0 (images):        in0 = src + p * n^2, no imaginary part
+//   map 1 (synthesis pair): p = b * J + jj, j = j0 + jj: in0 = c[b][2j], in1 = c[b][2j+1] (when < K)
+struct RowSrc {
+  int map;
+  int64_t J, j0, K;
+};
 template <class T, class R>
-__global__ void __launch_bounds__(kFftThreads)
-    rowifft_real_kernel(const typename Cx<R>::T* __restrict__ in, int64_t rows, int n, int logn,
-                        const typename Cx<R>::T* __restrict__ tw, R scale, int64_t q0, int64_t K,
-                        T* __restrict__ out, AdmmStore admm) {
+__global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src, const T* __restrict__ sub, RowSrc m,
+                                                       int logn, const typename Cx<R>::T* __restrict__ tw,
+                                                       typename Cx<R>::T* __restrict__ out) {
   using C = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* sm = reinterpret_cast<C*>(smraw);
-  const int nr = int(min(int64_t(blockDim.y), rows - int64_t(blockIdx.x) * blockDim.y));
-  const int64_t r0 = int64_t(blockIdx.x) * blockDim.y;
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y) {
-    const int r = e / n, c = e - r * n;
-    const C v = in[(r0 + r) * n + c];
-    sm[r * n + brev(c, logn)] = {v.x, -v.y};
+  const int n = 1 << logn;
+  const int64_t plane = int64_t(n) * n;
+  const int tile = tile_of(n), nr = tile / n;
+  const int64_t row0 = int64_t(blockIdx.x) * nr;  // global row over planes
+  const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
+  const T* in0;
+  const T* in1 = nullptr;
+  const T* s0 = nullptr;
+  const T* s1 = nullptr;
+  if (m.map == 0) {
+    in0 = src + p * plane;
+    if (sub) s0 = sub + p * plane;
+  } else {
+    const int64_t b = p / m.J, j = m.j0 + p % m.J, k0 = 2 * j;
+    in0 = src + (b * m.K + k0) * plane;
+    if (sub) s0 = sub + (b * m.K + k0) * plane;
+    if (k0 + 1 < m.K) {
+      in1 = in0 + plane;
+      if (sub) s1 = s0 + plane;
+    }
+  }
+  const int64_t base = lr0 * n;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    R re = ld_r<R>(in0 + base + e), im = R(0);
+    if (s0) re = re - ld_r<R>(s0 + base + e);  // sub(z1, u1) (admm.cpp:147)
+    if (in1) {
+      im = ld_r<R>(in1 + base + e);
+      if (s1) im = im - ld_r<R>(s1 + base + e);
+    }
+    sm[e] = {re, im};
   }
   __syncthreads();
-  fft_rows_smem(sm, nr, n, tw);
+  fft_dif(sm, nr, logn, n, tw);
+  C* o = out + p * plane + base;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) o[e] = sm[e];
+}
+
+// inverse row DIT of complex rows, scaled: Re -> out0, Im -> out1 (when present)
+// plane p -> destinations by `map`:
+//   map 0 (images):        out0 = dst + p * n^2
+//   map 1 (analysis pair): q = q0 + p, j = q / B, b = q % B: out0 = c[b][2j], out1 = c[b][2j+1] (when < K)
+struct RowDst {
+  int map;
+  int64_t q0, B, K;
+};
+template <class T, class R>
+__global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* __restrict__ in, RowDst m, int logn,
+                                                       const typename Cx<R>::T* __restrict__ tw, R scale,
+                                                       T* __restrict__ dst, AdmmStore admm) {
+  using C = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw);
+  const int n = 1 << logn;
   const int64_t plane = int64_t(n) * n;
-  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < nr * n; e += blockDim.x * blockDim.y) {
-    const int64_t idx = (r0 + e / n) * n + (e % n);
-    const R c = sm[e].x * scale;
+  const int tile = tile_of(n), nr = tile / n;
+  const int64_t row0 = int64_t(blockIdx.x) * nr;
+  const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
+  const int64_t base = lr0 * n;
+  const C* src = in + p * plane + base;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = src[e];
+  __syncthreads();
+  ifft_dit(sm, nr, logn, n, tw);
+  int64_t o0, o1 = -1;  // element offsets of the two output planes
+  int k0 = 0;
+  if (m.map == 0) {
+    o0 = p * plane;
+  } else {
+    const int64_t q = m.q0 + p, j = q / m.B, b = q % m.B;
+    k0 = int(2 * j);
+    o0 = (b * m.K + k0) * plane;
+    if (k0 + 1 < m.K) o1 = o0 + plane;
+  }
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    const C v = sm[e];
+    const R re = v.x * scale, im = v.y * scale;
     if (admm.z1 == nullptr) {
-      out[idx] = st_r<T>(c);
+      dst[o0 + base + e] = st_r<T>(re);
+      if (o1 >= 0) dst[o1 + base + e] = st_r<T>(im);
     } else {
-      const float cf = float(c);
-      const int64_t gi = q0 * plane + idx;  // global (image, coeff, row, col) index
-      const float u = admm.u1[gi];
-      const float z = soft(__fadd_rn(cf, u), admm.thresh[(q0 + idx / plane) % K]);
-      const float un = __fadd_rn(u, __fsub_rn(cf, z));
-      admm.z1[gi] = z;
-      admm.u1[gi] = un;
-      if (!isfinite(un)) atomicMin(admm.flag, admm.iteration);
+      admm_update(admm, o0 + base + e, k0, float(re));
+      if (o1 >= 0) admm_update(admm, o1 + base + e, k0 + 1, float(im));
     }
   }
 }
 
-// out[p][c][r] = in[p][r][c] (complex, tiled)
+// ---------------------------------------------------------------- column passes
+// A CTA owns `tc` adjacent columns of one plane (tc * n = tile elements),
+// staged column-major in shared memory with a padded stride.
+__host__ __device__ inline int col_ld(int n) { return n + 4; }
+
 template <class C>
-__global__ void transpose_c_kernel(const C* __restrict__ in, int nr, int nc, C* __restrict__ out) {
-  __shared__ C tile[32][33];
-  const int64_t plane = int64_t(nr) * nc;
-  const C* s = in + blockIdx.z * plane;
-  C* d = out + blockIdx.z * plane;
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int i = by + r, j = bx + threadIdx.x;
-    if (i < nr && j < nc) tile[r][threadIdx.x] = s[int64_t(i) * nc + j];
+__device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int n, int tc, int c0, int ld) {
+  for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
+    const int r = e / tc, c = e - r * tc;
+    sm[c * ld + r] = src[int64_t(r) * n + c0 + c];
   }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int i = bx + r, j = by + threadIdx.x;
-    if (i < nc && j < nr) d[int64_t(i) * nr + j] = tile[threadIdx.x][r];
+}
+template <class C>
+__device__ __forceinline__ void store_cols(C* __restrict__ dst, const C* sm, int n, int tc, int c0, int ld) {
+  for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
+    const int r = e / tc, c = e - r * tc;
+    dst[int64_t(r) * n + c0 + c] = sm[c * ld + r];
   }
 }
 
-struct Rows {
-  dim3 block;
-  unsigned grid;
-  size_t smem;
+// mode 0: out = colDIF(in)                          (plane p -> p)
+// mode 1: out = colDIT^-1(in[b] * (M_2j + i M_2j+1)) (analysis item q = q0 + p: j = q / B, b = q % B)
+// mode 2: out = colDIT^-1(in)                       (plane p -> p)
+template <class R>
+__global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __restrict__ in, int mode, int logn,
+                                                   const typename Cx<R>::T* __restrict__ tw,
+                                                   const typename Cx<R>::T* __restrict__ mult2, int64_t q0, int64_t B,
+                                                   typename Cx<R>::T* __restrict__ out) {
+  using C = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw);
+  const int n = 1 << logn, ld = col_ld(n);
+  const int64_t plane = int64_t(n) * n;
+  const int tile = tile_of(n), tc = tile / n;
+  const int tiles = n / tc;
+  const int64_t p = blockIdx.x / tiles;
+  const int c0 = int(blockIdx.x - p * tiles) * tc;
+  if (mode == 1) {
+    const int64_t q = q0 + p, j = q / B, b = q % B;
+    const C* src = in + b * plane;
+    const C* mk = mult2 + j * plane;
+    for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
+      const int r = e / tc, c = e - r * tc;
+      const int64_t gi = int64_t(r) * n + c0 + c;
+      sm[c * ld + r] = cmul(src[gi], mk[gi]);
+    }
+  } else {
+    load_cols(sm, in + p * plane, n, tc, c0, ld);
+  }
+  __syncthreads();
+  if (mode == 0)
+    fft_dif(sm, tc, logn, ld, tw);
+  else
+    ifft_dit(sm, tc, logn, ld, tw);
+  store_cols(out + p * plane, sm, n, tc, c0, ld);
+}
+
+// synthesis accumulation: for image b and a column tile, over the chunk's
+// pairs jj in ascending order: acc += colDIF(W[b][jj]) * (M_2j - i M_2j+1);
+// then S[b] += acc.  Each thread owns the same kPerThread tile elements
+// throughout, so the sum order per bin is fixed.
+template <class R>
+__global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* __restrict__ W, int64_t J, int64_t j0,
+                                                       int logn, const typename Cx<R>::T* __restrict__ tw,
+                                                       const typename Cx<R>::T* __restrict__ mult2,
+                                                       typename Cx<R>::T* __restrict__ S) {
+  using C = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw);
+  const int n = 1 << logn, ld = col_ld(n);
+  const int64_t plane = int64_t(n) * n;
+  const int tile = tile_of(n), tc = tile / n;
+  const int tiles = n / tc;
+  const int64_t b = blockIdx.x / tiles;
+  const int c0 = int(blockIdx.x - b * tiles) * tc;
+  C acc[kPerThread];
+#pragma unroll
+  for (int m = 0; m < kPerThread; ++m) acc[m] = {R(0), R(0)};
+  for (int64_t jj = 0; jj < J; ++jj) {
+    load_cols(sm, W + (b * J + jj) * plane, n, tc, c0, ld);
+    __syncthreads();
+    fft_dif(sm, tc, logn, ld, tw);
+    const C* mk = mult2 + (j0 + jj) * plane;
+#pragma unroll
+    for (int m = 0; m < kPerThread; ++m) {
+      const int e = threadIdx.x + m * blockDim.x;
+      if (e >= tile) break;
+      const int r = e / tc, c = e - r * tc;
+      const C v = cmul_conj(sm[c * ld + r], mk[int64_t(r) * n + c0 + c]);
+      acc[m] = {acc[m].x + v.x, acc[m].y + v.y};
+    }
+    __syncthreads();
+  }
+  C* s = S + b * plane;
+#pragma unroll
+  for (int m = 0; m < kPerThread; ++m) {
+    const int e = threadIdx.x + m * blockDim.x;
+    if (e >= tile) break;
+    const int r = e / tc, c = e - r * tc;
+    const int64_t gi = int64_t(r) * n + c0 + c;
+    const C a = s[gi];
+    s[gi] = {a.x + acc[m].x, a.y + acc[m].y};
+  }
+}
+
+// ---------------------------------------------------------------- host side
+int log2_of(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+struct Launch {
+  unsigned threads;
+  size_t row_smem, col_smem;
+  int tile, per_plane_rows, per_plane_cols;  // CTAs per plane in the row / column passes
 };
 template <class R>
-Rows rows_cfg(int64_t rows, int n) {
-  const size_t row_bytes = size_t(n) * sizeof(typename Cx<R>::T);
-  const int nr = int(std::max<size_t>(1, std::min<size_t>(8, 32768 / row_bytes)));  // rows per CTA
-  Rows c;
-  c.block = dim3(unsigned(kFftThreads / nr), unsigned(nr));
-  c.grid = unsigned((rows + nr - 1) / nr);
-  c.smem = size_t(nr) * row_bytes;
-  return c;
+Launch launch_cfg(int n) {
+  using C = typename Cx<R>::T;
+  Launch l;
+  l.tile = tile_of(n);
+  l.threads = unsigned(std::max(32, l.tile / kPerThread));
+  l.row_smem = size_t(l.tile) * sizeof(C);
+  const int tc = l.tile / n;
+  l.col_smem = size_t(tc) * size_t(col_ld(n)) * sizeof(C);
+  l.per_plane_rows = n / (l.tile / n);
+  l.per_plane_cols = n / tc;
+  return l;
 }
 
 template <class K>
@@ -253,102 +381,115 @@ void smem_opt_in(K kernel, size_t smem) {
   if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
 }
 
-template <class C>
-void transpose_c(const C* in, int64_t planes, int n, C* out, cudaStream_t st) {
-  dim3 grid(unsigned((n + 31) / 32), unsigned((n + 31) / 32), unsigned(planes));
-  KernelTimer t(RK_KERNEL_SHEARLET, st);
-  transpose_c_kernel<C><<<grid, dim3(32, 8), 0, st>>>(in, n, n, out);
-  RK_CUDA(cudaGetLastError());
-}
-
-template <class R>
-void c2c(const typename Cx<R>::T* in, int64_t rows, int n, int logn, const typename Cx<R>::T* tw, int mode,
-         const R* mult, int64_t q0, int64_t K, typename Cx<R>::T* out, cudaStream_t st) {
-  Rows c = rows_cfg<R>(rows, n);
-  smem_opt_in(rowfft_c2c_kernel<R>, c.smem);
-  KernelTimer t(RK_KERNEL_SHEARLET, st);
-  rowfft_c2c_kernel<R><<<c.grid, c.block, c.smem, st>>>(in, rows, n, logn, tw, mode, mult, q0, K, out);
-  RK_CUDA(cudaGetLastError());
-}
-
-int log2_of(int64_t n) {
-  int l = 0;
-  while ((int64_t(1) << l) < n) ++l;
-  return l;
-}
-
-// device tables in the working precision: fp32 ones are built with the plan,
-// fp64 ones on first use (multipliers transposed per coefficient)
 template <class R>
 struct Tables {
   const typename Cx<R>::T* tw;
-  const R* mult;
+  const typename Cx<R>::T* mult2;
 };
+
+// {M_2j, M_2j+1}[r][c] = M[brev r][brev c], zero for a missing odd partner
+template <class R>
+void build_tables(const Shearlet& sp, std::vector<typename Cx<R>::T>& mult2, std::vector<typename Cx<R>::T>& tw) {
+  const int64_t n = sp.height, bins = n * n, K = sp.n_coeff, P = (K + 1) / 2;
+  const int logn = log2_of(n);
+  std::vector<int64_t> rev(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t r = 0;
+    for (int bit = 0; bit < logn; ++bit)
+      if (i & (int64_t(1) << bit)) r |= int64_t(1) << (logn - 1 - bit);
+    rev[size_t(i)] = r;
+  }
+  mult2.assign(size_t(P * bins), {R(0), R(0)});
+  for (int64_t k = 0; k < K; ++k) {
+    const double* m = sp.multipliers.data() + k * bins;
+    auto* d = mult2.data() + (k / 2) * bins;
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c < n; ++c) {
+        const R v = R(m[rev[size_t(r)] * n + rev[size_t(c)]]);
+        if (k % 2 == 0)
+          d[r * n + c].x = v;
+        else
+          d[r * n + c].y = v;
+      }
+  }
+  tw.assign(size_t(std::max<int64_t>(n / 2, 1)), {R(0), R(0)});
+  for (int64_t k = 0; k < n / 2; ++k) {
+    const double ang = 2.0 * M_PI * double(k) / double(n);
+    tw[size_t(k)] = {R(std::cos(ang)), R(-std::sin(ang))};
+  }
+}
+
 template <class R>
 Tables<R> tables(Shearlet& sp);
 template <>
 Tables<float> tables<float>(Shearlet& sp) {
-  return {sp.d_twiddle.as<float2>(), sp.d_mult_t.as<float>()};
+  return {sp.d_twiddle.as<float2>(), sp.d_mult2.as<float2>()};
 }
 template <>
 Tables<double> tables<double>(Shearlet& sp) {
-  if (!sp.d_mult_t64.ptr) {
-    const int64_t h = sp.height, w = sp.width, bins = h * w;
-    std::vector<double> mt(size_t(sp.n_coeff * bins));
-    for (int64_t k = 0; k < sp.n_coeff; ++k)
-      for (int64_t i = 0; i < h; ++i)
-        for (int64_t j = 0; j < w; ++j) mt[size_t(k * bins + j * h + i)] = sp.multipliers[size_t(k * bins + i * w + j)];
-    std::vector<double2> tw(size_t(std::max<int64_t>(h / 2, 1)));
-    for (int64_t k = 0; k < h / 2; ++k) {
-      const double ang = 2.0 * M_PI * double(k) / double(h);
-      tw[size_t(k)] = make_double2(std::cos(ang), -std::sin(ang));
-    }
+  if (!sp.d_mult2_64.ptr) {
+    std::vector<double2> m2, tw;
+    build_tables<double>(sp, m2, tw);
     sp.d_twiddle64.reserve(tw.size() * sizeof(double2));
     RK_CUDA(cudaMemcpy(sp.d_twiddle64.ptr, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
-    sp.d_mult_t64.reserve(mt.size() * sizeof(double));
-    RK_CUDA(cudaMemcpy(sp.d_mult_t64.ptr, mt.data(), mt.size() * sizeof(double), cudaMemcpyHostToDevice));
+    sp.d_mult2_64.reserve(m2.size() * sizeof(double2));
+    RK_CUDA(cudaMemcpy(sp.d_mult2_64.ptr, m2.data(), m2.size() * sizeof(double2), cudaMemcpyHostToDevice));
   }
-  return {sp.d_twiddle64.as<double2>(), sp.d_mult_t64.as<double>()};
+  return {sp.d_twiddle64.as<double2>(), sp.d_mult2_64.as<double2>()};
+}
+
+template <class T, class R>
+void row_fwd(const T* src, const T* sub, RowSrc m, int64_t planes, int logn, const Launch& l,
+             const typename Cx<R>::T* tw, typename Cx<R>::T* out, cudaStream_t st) {
+  smem_opt_in(row_fwd_kernel<T, R>, l.row_smem);
+  KernelTimer t(RK_KERNEL_SHEARLET, st);
+  row_fwd_kernel<T, R><<<unsigned(planes * l.per_plane_rows), l.threads, l.row_smem, st>>>(src, sub, m, logn, tw, out);
+  RK_CUDA(cudaGetLastError());
+}
+
+template <class T, class R>
+void row_inv(const typename Cx<R>::T* in, RowDst m, int64_t planes, int logn, const Launch& l,
+             const typename Cx<R>::T* tw, R scale, T* dst, const AdmmStore& admm, cudaStream_t st) {
+  smem_opt_in(row_inv_kernel<T, R>, l.row_smem);
+  KernelTimer t(RK_KERNEL_SHEARLET, st);
+  row_inv_kernel<T, R><<<unsigned(planes * l.per_plane_rows), l.threads, l.row_smem, st>>>(in, m, logn, tw, scale, dst,
+                                                                                          admm);
+  RK_CUDA(cudaGetLastError());
+}
+
+template <class R>
+void col(const typename Cx<R>::T* in, int mode, int64_t planes, int logn, const Launch& l, const Tables<R>& tb,
+         int64_t q0, int64_t B, typename Cx<R>::T* out, cudaStream_t st) {
+  smem_opt_in(col_kernel<R>, l.col_smem);
+  KernelTimer t(RK_KERNEL_SHEARLET, st);
+  col_kernel<R><<<unsigned(planes * l.per_plane_cols), l.threads, l.col_smem, st>>>(in, mode, logn, tb.tw, tb.mult2,
+                                                                                     q0, B, out);
+  RK_CUDA(cudaGetLastError());
 }
 
 // shearlet.cpp:253-270: image [B][n][n] -> coefficients [B][K][n][n]
 template <class T, class R>
-void forward_impl(Shearlet& sp, const T* image, int64_t batch, T* coeff, AdmmStore admm, cudaStream_t st) {
+void forward_impl(Shearlet& sp, const T* image, int64_t batch, T* coeff, const AdmmStore& admm, cudaStream_t st) {
   using C = typename Cx<R>::T;
   const int n = int(sp.height), logn = log2_of(n);
-  const int64_t plane = int64_t(n) * n, K = sp.n_coeff;
+  const int64_t plane = int64_t(n) * n, K = sp.n_coeff, P = (K + 1) / 2;
   const Tables<R> tb = tables<R>(sp);
-  // (image, coeff) planes per chunk: two complex scratch planes each, ~32 MB
-  // in flight so the transpose and the last row pass hit L2
-  const int64_t total = batch * K;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(total, (int64_t(32) << 20) / (2 * plane * int64_t(sizeof(C)))));
-  sp.work_a.reserve(size_t(batch) * plane * sizeof(C));  // spectrum of every image, transposed
-  sp.work_b.reserve(size_t(std::max(chunk, batch)) * plane * sizeof(C) * 2);
+  const Launch l = launch_cfg<R>(n);
+  // (pair, image) items per chunk: the column pass's scratch planes, ~64 MB
+  const int64_t items = P * batch;
+  const int64_t chunk =
+      std::max<int64_t>(1, std::min<int64_t>(items, (int64_t(64) << 20) / (plane * int64_t(sizeof(C)))));
+  sp.work_a.reserve(size_t(batch) * plane * sizeof(C));  // X = fft2(x), bit-reversed order
+  sp.work_b.reserve(size_t(chunk) * plane * sizeof(C));
   C* X = sp.work_a.as<C>();
-  C* A = sp.work_b.as<C>();
-  C* Bt = A + size_t(std::max(chunk, batch)) * plane;
-  // X^T = columns-FFT(transpose(rows-FFT(x)))
-  {
-    Rows c = rows_cfg<R>(batch * n, n);
-    smem_opt_in(rowfft_real_kernel<T, R>, c.smem);
-    KernelTimer t(RK_KERNEL_SHEARLET, st);
-    rowfft_real_kernel<T, R><<<c.grid, c.block, c.smem, st>>>(image, nullptr, plane, batch * n, n, logn, tb.tw, A);
-    RK_CUDA(cudaGetLastError());
-  }
-  transpose_c(A, batch, n, Bt, st);
-  c2c<R>(Bt, batch * n, n, logn, tb.tw, 0, nullptr, 0, 1, X, st);
+  C* Wk = sp.work_b.as<C>();
+  row_fwd<T, R>(image, nullptr, RowSrc{0, 1, 0, K}, batch, logn, l, tb.tw, X, st);
+  col<R>(X, 0, batch, logn, l, tb, 0, 1, X, st);
   const R scale = R(1) / R(plane);
-  for (int64_t q0 = 0; q0 < total; q0 += chunk) {
-    const int64_t planes = std::min(chunk, total - q0);
-    // inverse along columns of X^T * M_k^T (rows of the transposed layout)
-    c2c<R>(X, planes * n, n, logn, tb.tw, 1, tb.mult, q0, K, A, st);
-    transpose_c(A, planes, n, Bt, st);
-    Rows c = rows_cfg<R>(planes * n, n);
-    smem_opt_in(rowifft_real_kernel<T, R>, c.smem);
-    KernelTimer t(RK_KERNEL_SHEARLET, st);
-    rowifft_real_kernel<T, R><<<c.grid, c.block, c.smem, st>>>(Bt, planes * n, n, logn, tb.tw, scale, q0, K,
-                                                               coeff ? coeff + q0 * plane : nullptr, admm);
-    RK_CUDA(cudaGetLastError());
+  for (int64_t q0 = 0; q0 < items; q0 += chunk) {
+    const int64_t nq = std::min(chunk, items - q0);
+    col<R>(X, 1, nq, logn, l, tb, q0, batch, Wk, st);
+    row_inv<T, R>(Wk, RowDst{1, q0, batch, K}, nq, logn, l, tb.tw, scale, coeff, admm, st);
   }
 }
 
@@ -357,38 +498,41 @@ template <class T, class R>
 void backward_impl(Shearlet& sp, const T* coeff, const T* sub, int64_t batch, T* image, cudaStream_t st) {
   using C = typename Cx<R>::T;
   const int n = int(sp.height), logn = log2_of(n);
-  const int64_t plane = int64_t(n) * n, K = sp.n_coeff;
+  const int64_t plane = int64_t(n) * n, K = sp.n_coeff, P = (K + 1) / 2;
   const Tables<R> tb = tables<R>(sp);
+  const Launch l = launch_cfg<R>(n);
+  const int64_t J = std::min<int64_t>(kPairChunk, P);
   sp.work_a.reserve(size_t(batch) * plane * sizeof(C));
-  sp.work_b.reserve(size_t(batch) * plane * sizeof(C) * 2);
-  C* S = sp.work_a.as<C>();  // accumulated spectrum, transposed
-  C* A = sp.work_b.as<C>();
-  C* Bt = A + size_t(batch) * plane;
+  sp.work_b.reserve(size_t(batch) * size_t(J) * plane * sizeof(C));
+  C* S = sp.work_a.as<C>();  // accumulated spectrum, bit-reversed order
+  C* Wk = sp.work_b.as<C>();
   RK_CUDA(cudaMemsetAsync(S, 0, size_t(batch) * plane * sizeof(C), st));
-  Rows c = rows_cfg<R>(batch * n, n);
-  smem_opt_in(rowfft_real_kernel<T, R>, c.smem);
-  for (int64_t k = 0; k < K; ++k) {  // ascending k: a fixed reduction order (shearlet.cpp:286-291)
-    {
-      KernelTimer t(RK_KERNEL_SHEARLET, st);
-      rowfft_real_kernel<T, R><<<c.grid, c.block, c.smem, st>>>(coeff + k * plane, sub ? sub + k * plane : nullptr,
-                                                                K * plane, batch * n, n, logn, tb.tw, A);
-      RK_CUDA(cudaGetLastError());
-    }
-    transpose_c(A, batch, n, Bt, st);
-    // forward along columns, S += result * M_k^T
-    c2c<R>(Bt, batch * n, n, logn, tb.tw, 2, tb.mult, k, K, S, st);
+  smem_opt_in(col_acc_kernel<R>, l.col_smem);
+  for (int64_t j0 = 0; j0 < P; j0 += J) {  // ascending pairs: a fixed reduction order
+    const int64_t nj = std::min(J, P - j0);
+    row_fwd<T, R>(coeff, sub, RowSrc{1, nj, j0, K}, batch * nj, logn, l, tb.tw, Wk, st);
+    KernelTimer t(RK_KERNEL_SHEARLET, st);
+    col_acc_kernel<R><<<unsigned(batch * l.per_plane_cols), l.threads, l.col_smem, st>>>(Wk, nj, j0, logn, tb.tw,
+                                                                                         tb.mult2, S);
+    RK_CUDA(cudaGetLastError());
   }
   // image = Re(ifft2(S)) / (n n)
-  c2c<R>(S, batch * n, n, logn, tb.tw, 3, nullptr, 0, 1, A, st);
-  transpose_c(A, batch, n, Bt, st);
-  smem_opt_in(rowifft_real_kernel<T, R>, c.smem);
-  KernelTimer t(RK_KERNEL_SHEARLET, st);
-  rowifft_real_kernel<T, R><<<c.grid, c.block, c.smem, st>>>(Bt, batch * n, n, logn, tb.tw, R(1) / R(plane), 0, 1,
-                                                             image, AdmmStore{});
-  RK_CUDA(cudaGetLastError());
+  col<R>(S, 2, batch, logn, l, tb, 0, 1, Wk, st);
+  row_inv<T, R>(Wk, RowDst{0, 0, 1, 1}, batch, logn, l, tb.tw, R(1) / R(plane), image, AdmmStore{}, st);
 }
 
 }  // namespace
+
+void upload_shearlet(Shearlet& sp) {
+  if (sp.device < 0) return;
+  std::vector<float2> m2, tw;
+  build_tables<float>(sp, m2, tw);
+  RK_CUDA(cudaSetDevice(sp.device));
+  sp.d_mult2.reserve(m2.size() * sizeof(float2));
+  sp.d_twiddle.reserve(tw.size() * sizeof(float2));
+  RK_CUDA(cudaMemcpy(sp.d_mult2.ptr, m2.data(), m2.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(sp.d_twiddle.ptr, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+}
 
 void shearlet_forward(Shearlet& sp, int dtype, const void* image, int64_t batch, void* coeff, cudaStream_t st) {
   switch (dtype) {

@@ -3,7 +3,7 @@
 // cone-adapted real-valued windows (Meyer-type radial bands x directional
 // bumps), exact evenness under frequency negation, joint Parseval
 // normalisation.  The device applies them with the 2-D FFT kernels of
-// shearlet.cu.
+// shearlet.cu (upload_shearlet builds the device tables there).
 #include <algorithm>
 #include <cmath>
 
@@ -144,28 +144,6 @@ void build_shearlet(Shearlet& sp, int64_t height, int64_t width, const std::vect
   for (int64_t k = 0; k < sp.n_coeff; ++k)
     for (int64_t b = 0; b < bins; ++b) mult[size_t(k * bins + b)] *= ssum[size_t(b)];
   upload_shearlet(sp);
-}
-
-void upload_shearlet(Shearlet& sp) {
-  if (sp.device < 0) return;
-  const int64_t h = sp.height, w = sp.width, bins = h * w;
-  const std::vector<double>& mult = sp.multipliers;
-  // device copies: multipliers in the transposed (column-major) layout the
-  // 2-D FFT pipeline keeps its spectra in, fp32; forward twiddles of length h
-  std::vector<float> mt(size_t(sp.n_coeff * bins));
-  for (int64_t k = 0; k < sp.n_coeff; ++k)
-    for (int64_t i = 0; i < h; ++i)
-      for (int64_t j = 0; j < w; ++j) mt[size_t(k * bins + j * h + i)] = float(mult[size_t(k * bins + i * w + j)]);
-  std::vector<float2> tw(static_cast<size_t>(std::max<int64_t>(h / 2, 1)));
-  for (int64_t k = 0; k < h / 2; ++k) {
-    const double ang = 2.0 * M_PI * double(k) / double(h);
-    tw[size_t(k)] = make_float2(float(std::cos(ang)), float(-std::sin(ang)));
-  }
-  RK_CUDA(cudaSetDevice(sp.device));
-  sp.d_mult_t.reserve(mt.size() * sizeof(float));
-  sp.d_twiddle.reserve(tw.size() * sizeof(float2));
-  RK_CUDA(cudaMemcpy(sp.d_mult_t.ptr, mt.data(), mt.size() * sizeof(float), cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(sp.d_twiddle.ptr, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
 }
 
 }  // namespace rk

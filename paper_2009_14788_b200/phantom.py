@@ -12,9 +12,10 @@ _SL = [(1.0, 0.69, 0.92, 0.0, 0.0, 0.0), (-0.8, 0.6624, 0.874, 0.0, -0.0184, 0.0
        (0.1, 0.023, 0.046, 0.06, -0.605, 0.0)]
 
 
-def shepp_logan(s):
+def shepp_logan(s, dtype=np.float32):
     """Synthetic input: modified Shepp-Logan (the reference's table, phantom.cpp:18-29)
-    rasterised at 400^2 and bilinearly resampled to s^2 (phantom.cpp:61-101), numpy."""
+    rasterised at 400^2 and bilinearly resampled to s^2 (phantom.cpp:61-101), numpy;
+    computed in double and narrowed like Tensor::from_double_as (half via float)."""
     base = 400
     y = (base - 1 - 2 * np.arange(base))[:, None] / base
     x = (2 * np.arange(base) + 1 - base)[None, :] / base
@@ -30,6 +31,11 @@ def shepp_logan(s):
     i1 = np.minimum(i0 + 1, base - 1)
     top = (1 - f)[None, :] * img[i0][:, i0] + f[None, :] * img[i0][:, i1]
     bot = (1 - f)[None, :] * img[i1][:, i0] + f[None, :] * img[i1][:, i1]
-    return ((1 - f)[:, None] * top + f[:, None] * bot).astype(np.float32)
+    out = (1 - f)[:, None] * top + f[:, None] * bot
+    dtype = np.dtype(dtype)
+    if dtype == np.float64:
+        return out
+    out = out.astype(np.float32)
+    return out if dtype == np.float32 else out.astype(dtype)
 
 

@@ -57,3 +57,69 @@ def test_cli_pipeline(tmp_path, oracle, cuda):
     for key in ("version", "geometry", "batch", "precision", "warmup", "runs", "threads", "forward", "backprojection"):
         assert key in b
     assert len(b["forward"]["runs_ms"]) == 5 and b["forward"]["images_per_s"] > 0
+
+
+def test_cli_phantom_matches_reference(tmp_path, ref):
+    """phantom subcommand (cli.cpp:233-251) writes the reference's phantom bit for bit."""
+    for prec, dt in (("single", np.float32), ("double", np.float64), ("half", np.float16)):
+        r = cli("phantom", "--size", "64", "--precision", prec, "-o", str(tmp_path / f"p_{prec}.npy"))
+        assert r.returncode == 0, r.stderr
+        got = np.load(tmp_path / f"p_{prec}.npy")
+        assert got.dtype == dt and got.shape == (64, 64)
+        assert np.array_equal(got, ref.shepp_logan(64, dt)[0])
+
+
+def test_npy_golden_bytes(tmp_path):
+    """The .npy files the CLI writes are byte-identical to the reference's frozen
+    numpy goldens (test_npy.cpp:19-35), and read back exactly (:39-71)."""
+    hdr = "934e554d5059010076007b276465736372273a20273c66{}272c2027666f727472616e5f6f72646572273a2046616c73652c20"
+    golden = [
+        (hdr.format("34") + "277368617065273a2028322c2033292c207d" + "20" * 58 + "0a"
+         "0000c03f000010c0000000000000484000009040000060bf", np.array([[1.5, -2.25, 0.0], [3.125, 4.5, -0.875]], np.float32)),
+        (hdr.format("38") + "277368617065273a2028332c292c207d" + "20" * 60 + "0a"
+         "9a9999999999b93f9a9999999999c9bf333333333333d33f", np.array([0.1, -0.2, 0.3], np.float64)),
+        (hdr.format("32") + "277368617065273a2028322c2032292c207d" + "20" * 58 + "0a" "003c00b800340040",
+         np.array([[1.0, -0.5], [0.25, 2.0]], np.float16)),
+    ]
+    from paper_2009_14788_b200.cli import _read, _write
+
+    for k, (hexs, vals) in enumerate(golden):
+        p = tmp_path / f"g{k}.npy"
+        _write(str(p), vals)
+        assert p.read_bytes() == bytes.fromhex(hexs), vals.dtype
+        back = np.load(p)
+        assert back.dtype == vals.dtype and np.array_equal(back, vals)
+        if vals.ndim == 2:
+            assert np.array_equal(_read(str(p), 3)[0], vals)
+
+
+@pytest.mark.gpu
+def test_cli_shearlet_and_admm(tmp_path, ref, cuda):
+    """shearlet (cli.cpp:440-476) round trip and admm (cli.cpp:478-556) JSON report."""
+    import math
+
+    from paper_2009_14788_b200.phantom import shepp_logan
+
+    ph = shepp_logan(32)
+    np.save(tmp_path / "ph.npy", ph)
+    r = cli("shearlet", "--scales", "3", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "c.npy"))
+    assert r.returncode == 0, r.stderr
+    c = np.load(tmp_path / "c.npy")
+    assert c.shape == (27, 32, 32)
+    assert np.abs(c - ref.shearlet_forward(ph[None], [0.5] * 3)[0]).max() < 1e-5
+    r = cli("shearlet", "--scales", "3", "--inverse", "--in", str(tmp_path / "c.npy"), "-o", str(tmp_path / "x.npy"))
+    assert r.returncode == 0 and np.abs(np.load(tmp_path / "x.npy") - ph).max() < 1e-5
+    r = cli("shearlet", "--scales", "2", "--inverse", "--in", str(tmp_path / "c.npy"), "-o", str(tmp_path / "y.npy"))
+    assert r.returncode == 1 and "coefficient count" in r.stderr
+    ang = [(i * 100.0 / 32 - 50.0) * math.pi / 180.0 for i in range(32)]
+    import paper_2009_14788_b200 as rk
+    import torch
+
+    y = rk.forward(rk.make_parallel(32, ang), torch.from_numpy(ph[None]).cuda()).cpu().numpy()[0]
+    np.save(tmp_path / "y.npy", y)
+    r = cli("--json", "admm", "--size", "32", "--angles-range", "100", "--scales", "3", "--outer", "20", "--in",
+            str(tmp_path / "y.npy"), "-o", str(tmp_path / "rec.npy"), "--reference", str(tmp_path / "ph.npy"))
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["command"] == "admm" and rep["outer"] == 20 and rep["mse_vs_reference"] < 1.5e-2
+    assert rep["geometry"]["n_angles"] == 32
