@@ -443,6 +443,29 @@ def measure_extras(rk, _lib, dev):
     ms = timed(lambda: rk.cgne(op, z, y, 50), runs=1)
     out["cfg5_cgne50_512_256_b256"] = {"metric": "reconstructed images/s (50 iterations)", "value": 256 / (ms * 1e-3),
                                        "ms": ms}
+    del x, y, z
+    # alpha-shearlet analysis / synthesis, 512^2, 5 scales at alpha 0.5 (59 coefficients), batch 8
+    plan = rk.make_plan(512, 512, [0.5] * 5)
+    x = torch.from_numpy(np.stack([rk_phantom(512) * ((e + 1) / 8.0) for e in range(8)])).to(dev)
+    c = rk.forward(plan, x)
+    ms_f = timed(lambda: rk.forward(plan, x))
+    ms_b = timed(lambda: rk.backward(plan, c))
+    out["next_shearlet512_s5_b8_fp32"] = {"metric": "shearlet analysis / synthesis images/s", "forward": 8 / (ms_f * 1e-3),
+                                          "backward": 8 / (ms_b * 1e-3), "ms_forward": ms_f, "ms_backward": ms_b,
+                                          "n_coeff": plan.n_coeff}
+    del c
+    # the paper's ADMM: 512^2, limited 100 degree arc, 512 angles,
+    # 5 scales, p0 0.02, p1 0.1, 50 outer x 50 inner iterations; batch 1 and 8
+    ga = rk.make_parallel(512, [(i * 100.0 / 512 - 50.0) * math.pi / 180.0 for i in range(512)])
+    opa = rk.projector_operator(ga)
+    for b in (1, 8):
+        ya = rk.forward(ga, x[:b])
+        rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=1))  # warm-up (plans, scratch)
+        ms = timed(lambda: rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=50,
+                                                                             inner_cg_iterations=50)), runs=1)
+        out[f"next_admm512_limited100_na512_b{b}_fp32"] = {"metric": "ADMM seconds per image (50 outer x 50 inner)",
+                                                           "value": ms * 1e-3 / b, "ms": ms,
+                                                           "paper_v100_s_per_image": 1.6 if b == 1 else 1.2}
     return out
 
 
