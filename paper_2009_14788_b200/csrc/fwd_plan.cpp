@@ -85,6 +85,18 @@ double conflict_cost(const std::vector<Pt>& lanes_at_step, bool transposed, int 
   return cost;
 }
 
+// Conflict-free reference for conflict_cost: one wavefront per quarter warp
+// and tap with at least one active lane.
+double ideal_cost(const std::vector<Pt>& lanes_at_step) {
+  double cost = 0.0;
+  for (size_t q = 0; q + 8 <= lanes_at_step.size(); q += 8) {
+    bool any = false;
+    for (size_t l = 0; l < 8; ++l) any |= !std::isnan(lanes_at_step[q + l].px);
+    cost += any ? 4.0 : 0.0;
+  }
+  return cost;
+}
+
 struct Box {
   int64_t r0, c0, rows, cols;  // normal (untransposed) padded-image coordinates
   bool empty() const { return rows <= 0; }
@@ -228,6 +240,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     int tr = 0, residue = 0, swap = 0, mapping = 0;
     bool ok = false;
     int64_t staged = 0, max_cells = 0;
+    double cost = 0.0, ideal = 0.0;  // simulated wavefronts: chosen layout, conflict-free
     std::vector<int4> boxes;
   };
   auto plan_shape = [&](Shape sh, std::vector<CtaPlan>& plans) {
@@ -239,24 +252,27 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       for (int cta = lo; cta < hi; ++cta) {
         const int2* wa = &warps[size_t(cta) * 8];
         CtaPlan& cp = plans[size_t(cta)];
-        // lane positions at a few aligned steps of the march
-        // Two lane mappings: detector-major (warp = one angle, lanes = 32 cells) and,
-        // for a full 8-angle x 32-cell CTA, angle-major (warp w = cells 4w..4w+3,
-        // lane l = angle slot l & 7, cell 4w + l / 8): a quarter warp then reads
-        // one cell's 8 neighbouring angles, points on a short arc that often share
-        // texels.  Positions at a few aligned steps of the march, in lane order.
+        // Lane mappings (kernels.cu): a quarter warp covers 2^lq neighbouring
+        // angle slots x 8 >> lq neighbouring cells; lq = 0 (detector-major) is
+        // the only one for partial CTA shapes.  Near-parallel lines of one
+        // angle and short arcs of one cell's neighbouring angles conflict at
+        // different directions, so each CTA takes the cheapest.  Positions at
+        // a few aligned steps of the march, in lane order.
         const bool full8 = sh.aa == 8 && sh.db == 1;
-        auto lane_ray = [&](int mapping, int w, int l, int& a_out, int64_t& k_out) {
-          if (mapping == 0) {
+        auto lane_ray = [&](int lq, int w, int l, int& a_out, int64_t& k_out) {
+          if (lq == 0) {
             a_out = wa[w].x;
             k_out = int64_t(wa[w].y) + l;
-          } else {
-            a_out = wa[l & 7].x;
-            k_out = int64_t(wa[0].y) + 4 * w + (l >> 3);
+            return;
           }
+          const int t = w * 32 + l;
+          const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
+          const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
+          a_out = wa[(ag << lq) + aq].x;
+          k_out = int64_t(wa[0].y) + cg * (8 >> lq) + cq;
         };
         double best = 1e300;
-        for (int mapping = 0; mapping < (full8 ? 2 : 1); ++mapping) {
+        for (int mapping = 0; mapping < (full8 ? 4 : 1); ++mapping) {
           sim.clear();
           for (int st = 0; st < 8; ++st) {
             const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st) / 7.0);
@@ -283,8 +299,10 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
                 const double c = conflict_cost(sim, tr == 1, 64 + res, swap) *
                                  (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
                 if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap, cp.mapping = mapping;
+                if (mapping == 0 && tr == 0 && swap == 0 && res == 0) cp.ideal = ideal_cost(sim);
               }
         }
+        cp.cost = best;
         cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
       }
     };
@@ -324,18 +342,25 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     F.max_box = 0;
     F.staged_texels = 0;
     F.any_transposed = false;
+    F.sim_cost = F.sim_ideal = 0.0;
+    for (int& mc : F.mapping_count) mc = 0;
     for (size_t c = 0; c < plans.size(); ++c) {
       const CtaPlan& cp = plans[c];
       F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()), cp.tr | (cp.swap << 1) | (cp.mapping << 3), 0);
+      F.sim_cost += cp.cost;
+      F.sim_ideal += cp.ideal;
+      F.mapping_count[cp.mapping & 3] += 1;
       F.boxes.insert(F.boxes.end(), cp.boxes.begin(), cp.boxes.end());
       F.max_box = std::max(F.max_box, cp.max_cells);
       F.staged_texels += cp.staged;
       F.any_transposed |= cp.tr == 1;
     }
     if (std::getenv("RK_DEBUG_PLAN")) {
-      int64_t ntr = 0, nam = 0;
-      for (const int4& c : F.cta) ntr += c.z & 1, nam += (c.z >> 3) & 1;
-      std::fprintf(stderr, "[rk] forward schedule: %lld CTAs angle-major\n", (long long)nam);
+      int64_t ntr = 0;
+      for (const int4& c : F.cta) ntr += c.z & 1;
+      std::fprintf(stderr, "[rk] forward schedule: lane mappings (angles per quarter warp 1/2/4/8) %d/%d/%d/%d CTAs, "
+                   "simulated wavefronts %.3fx conflict-free\n", F.mapping_count[0], F.mapping_count[1],
+                   F.mapping_count[2], F.mapping_count[3], F.sim_cost / std::max(F.sim_ideal, 1.0));
       std::fprintf(stderr,
                    "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
                    "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",

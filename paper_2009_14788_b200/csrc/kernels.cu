@@ -164,13 +164,23 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
   const int64_t g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 cfg = __ldg(cta_cfg + cta);  // {first box, boxes, flags}
-  // lane -> ray: detector-major (warp = angle slot, lane = cell) or angle-major
-  // (lane & 7 = angle slot, cell 4 warp + lane / 8), chosen by the planner
-  // against bank conflicts; angles are sorted by direction
-  const bool amaj = ((cfg.z >> 3) & 1) != 0;
-  const int2 wa = __ldg(warps + cta * (kFwdThreads / 32) + (amaj ? (lane & 7) : warp));
-  const int a = wa.x;
-  const int k = amaj ? __ldg(warps + cta * (kFwdThreads / 32)).y + 4 * warp + (lane >> 3) : wa.y + lane;
+  // lane -> ray, chosen by the planner against bank conflicts (angles are
+  // sorted by direction).  A quarter warp (8 lanes, one shared-memory
+  // wavefront per 128-bit load) covers 2^lq neighbouring angles x 8 >> lq
+  // neighbouring cells: lq = 0 detector-major (warp = angle slot, lane = cell;
+  // any CTA shape), lq = 3 angle-major (one cell's 8 angles); 1, 2 mixed.
+  const int lq = (cfg.z >> 3) & 3;
+  int slot = warp, k;
+  if (lq == 0) {
+    k = __ldg(warps + cta * (kFwdThreads / 32) + warp).y + lane;
+  } else {
+    const int t = threadIdx.x;
+    const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
+    const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
+    slot = (ag << lq) + aq;
+    k = __ldg(warps + cta * (kFwdThreads / 32)).y + cg * (8 >> lq) + cq;
+  }
+  const int a = __ldg(warps + cta * (kFwdThreads / 32) + slot).x;
   const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
   const bool tr = (cfg.z & 1) != 0;

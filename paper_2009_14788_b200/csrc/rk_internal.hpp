@@ -76,10 +76,12 @@ struct ForwardSchedule {
   int64_t max_box = 0;             // largest rows * pitch over all boxes (float4 cells)
   int64_t staged_texels = 0;       // per image group, all CTAs and chunks
   bool any_transposed = false;
+  double sim_cost = 0.0, sim_ideal = 0.0;  // planner's simulated shared-memory wavefronts (chosen, conflict-free)
+  int mapping_count[4] = {0, 0, 0, 0};      // CTAs per lane mapping (log2 angles per quarter warp)
   // per chunk {row0 | col0 << 16, rows | cols << 16, pitch, t_end (float bits; inf = last)},
   // in staged-image coordinates, CTA after CTA
   std::vector<int4> boxes;
-  std::vector<int4> cta;    // per CTA {first box, box count, bit0 transposed | bits1-2 lane tap order, 0}
+  std::vector<int4> cta;    // per CTA {first box, box count, bit0 transposed | bits1-2 lane tap order | bits3-4 lane mapping, 0}
   std::vector<int2> warps;  // per CTA x 8 warps {angle (-1: idle), first detector cell}
 };
 
