@@ -318,19 +318,23 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 constexpr int kTile = 32;
+constexpr int kMaxBpChunk = 32;  // angles per staging pass (one constants record per thread of the first warp)
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 
 template <int KIND, class TOut>
 __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
-    double det_distance, const double2* __restrict__ trig, int window, int chunk, int64_t batch,
-    TOut* __restrict__ out, BpEpilogue epi) {
+    double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
+    int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
   extern __shared__ float4 smem[];
-  float4* win = smem;                                                    // chunk * window cells
-  Const* cst = reinterpret_cast<Const*>(smem + size_t(chunk) * window);  // chunk records
-  int* ws_s = reinterpret_cast<int*>(cst + chunk);                        // chunk window starts
+  // this tile's staged cells per angle, and as many angles per pass as fit
+  const int window = __ldg(tile_window + blockIdx.y * gridDim.x + blockIdx.x);
+  const int chunk = min(kMaxBpChunk, cells / window);
+  float4* win = smem;                                                  // chunk * window <= cells
+  Const* cst = reinterpret_cast<Const*>(smem + cells);                 // kMaxBpChunk records
+  int* ws_s = reinterpret_cast<int*>(cst + kMaxBpChunk);               // kMaxBpChunk window starts
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kTile + tx;
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile;
@@ -548,7 +552,7 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
   dim3 block(kTile, kTile / kRowsPerThread);
   const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
   const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
-  const size_t smem = size_t(p.bp_angle_chunk) * p.bp_window * sizeof(float4) + size_t(p.bp_angle_chunk) * (rec + sizeof(int));
+  const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     auto kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T>
@@ -556,8 +560,8 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
-                                    p.g.source_distance, p.g.det_distance, p.trig.as<double2>(), p.bp_window,
-                                    p.bp_angle_chunk, batch, static_cast<T*>(image), epi);
+                                    p.g.source_distance, p.g.det_distance, p.trig.as<double2>(),
+                                    p.bp_tile_window.as<int>(), p.bp_cells, batch, static_cast<T*>(image), epi);
   });
   RK_CUDA(cudaGetLastError());
 }

@@ -171,7 +171,9 @@ void build_plan(Plan& p) {
   const double off = 0.5 * double(nd) - 0.5;
   const double span = g.source_distance + g.det_distance;
   int64_t tiles = (s + kBpTile - 1) / kBpTile;
-  int64_t need = 0;
+  // per tile: the widest footprint over all angles (fan beam: tiles far from
+  // the source need far fewer cells than the ones next to it)
+  std::vector<int64_t> tile_need(size_t(tiles * tiles), 0);
   for (int64_t a = 0; a < na; ++a) {
     double c = trig[size_t(a)].x, sn = trig[size_t(a)].y;
     for (int64_t ty = 0; ty < tiles; ++ty) {
@@ -197,18 +199,25 @@ void build_plan(Plan& p) {
         // clamp lands on the two zero cells at the clipped end
         int64_t ws = std::max<int64_t>(int64_t(std::floor(lo)) - 1, -2);
         int64_t we = std::min<int64_t>(int64_t(std::floor(hi)) + 2, nd + 1);
-        need = std::max(need, we - ws + 1);
+        int64_t& tn = tile_need[size_t(ty * tiles + tx)];
+        tn = std::max(tn, we - ws + 1);
       }
       if (!fan) break;  // parallel: footprint width is translation invariant up to floor effects
     }
   }
-  if (!fan) need += 1;  // floor effects across tiles
-  need += 1;            // rounding margin
-  int64_t window = (need + 3) / 4 * 4;
+  int64_t need = 0;
+  for (int64_t t = 0; t < tiles * tiles; ++t) need = std::max(need, tile_need[size_t(t)]);
+  // + floor effects across tiles (parallel) + a rounding margin (the kernel
+  // derives each angle's window start in its own fp64 arithmetic)
+  auto padded_window = [&](int64_t n) { return (n + (fan ? 1 : 2) + 3) / 4 * 4; };
+  int64_t window = padded_window(need);
   if (window > 12 * 1024)
     throw ValidationError("backprojection window of " + std::to_string(window) +
                           " detector cells exceeds shared memory (det_count too large)");
   p.bp_window = int(window);
+  std::vector<int> tile_window(size_t(tiles * tiles));
+  for (int64_t t = 0; t < tiles * tiles; ++t)
+    tile_window[size_t(t)] = int(fan ? padded_window(tile_need[size_t(t)]) : window);
   // fp32 (tile-relative) fan map unless the magnification span / (sp (D_so - R))
   // of the pixels nearest the source is large (kernels.cu, kBpFan32 / kBpFan64)
   if (fan) {
@@ -216,9 +225,12 @@ void build_plan(Plan& p) {
     const double mag = span / (g.det_spacing * (g.source_distance - rmax));
     p.bp_fan_fp64 = !(mag <= 8.0);
   }
-  // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to 192 KB)
+  // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to
+  // 192 KB) for the widest tile; narrower tiles stage more angles per pass in
+  // the same cells (kernels.cu: chunk = min(32, cells / tile window))
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(32, (32 * 1024) / (window * 16)));
   p.bp_angle_chunk = int(chunk);
+  p.bp_cells = int(chunk * window);
 
   // ----- upload (device < 0: host-only plan, used for inspection on machines without a GPU)
   if (p.device < 0) return;
@@ -235,6 +247,9 @@ void build_plan(Plan& p) {
   p.fwd_warps.reserve(p.fwd.warps.size() * sizeof(int2));
   RK_CUDA(cudaMemcpy(p.fwd_warps.ptr, p.fwd.warps.data(), p.fwd.warps.size() * sizeof(int2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  p.bp_tile_window.reserve(tile_window.size() * sizeof(int));
+  RK_CUDA(cudaMemcpy(p.bp_tile_window.ptr, tile_window.data(), tile_window.size() * sizeof(int),
+                     cudaMemcpyHostToDevice));
   RK_CUDA(cudaEventCreateWithFlags(&p.scratch_free, cudaEventDisableTiming));
 }
 

@@ -109,8 +109,10 @@ struct Plan {
   DeviceBuffer fwd_warps;  // int2 {angle, first detector} per (cta, warp); angle -1 = idle
   // backprojection: per-angle trig in fp64
   DeviceBuffer trig;       // double2 {cos, sin}
-  int bp_window = 0;       // staged detector cells per (tile, angle)
-  int bp_angle_chunk = 0;  // angles staged per pass
+  int bp_window = 0;       // staged detector cells per (tile, angle), widest tile
+  int bp_angle_chunk = 0;  // angles staged per pass, widest tile
+  int bp_cells = 0;        // staged cells per pass (shared memory), all tiles
+  DeviceBuffer bp_tile_window;  // int per 32x32 tile: its staged cells per angle
   bool bp_fan_fp64 = false;  // fan beam with the source close to the image: fp64 pixel map
 
   // scratch (serialised by `mu`; `scratch_free` orders reuse across streams)

@@ -13,3 +13,10 @@ d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 pk = d["roofline"]["per_kernel"]
 print(f"{d['value']:.0f} img/s  e2e {d['e2e']['value']:.0f}  fwd {pk['forward']['ms']:.3f} ms  bp {pk['backproject']['ms']:.3f} ms  frac {d['roofline']['frac']:.3f} clocks {d['clocks']}")
 PY
+timeout 300 python bench.py --workload fan512 --no-cpu-baseline --no-extras --no-e2e > gpurun_out/bench_${TAG}_fan.json 2> gpurun_out/bench_${TAG}_fan.err
+python - gpurun_out/bench_${TAG}_fan.json <<'PY'
+import json, sys
+d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+pk = d["roofline"]["per_kernel"]
+print(f"fan512: {d['value']:.0f} img/s  fwd {pk['forward']['ms']:.3f} ms  bp {pk['backproject']['ms']:.3f} ms")
+PY
