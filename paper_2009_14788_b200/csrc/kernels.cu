@@ -8,6 +8,7 @@
 // equal per-element results bit for bit (acceptance.cpp:340-389).
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "rk_internal.hpp"
@@ -153,7 +154,13 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // the boxes carry one unit of slack in t, so rounding never leaves a sample
 // outside its box.  CTAs whose lanes spread mostly along image columns read
 // the transposed packed image with x and y swapped (bilinear is symmetric).
-template <class TOut>
+//
+// LANE (batch 1): only lane 0 of the packed group carries an image, so the box
+// is staged as scalars (lane 0 of each texel, cooperative 16-byte loads) and
+// every tap is a 32-bit shared load: a quarter of the shared-memory traffic
+// and FMAs of the packed loop, with the same operations on lane 0 in the same
+// order, so its results equal the packed kernel's bit for bit.
+template <class TOut, bool LANE>
 __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
@@ -220,14 +227,24 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const int m_end =
         isinf(tend) ? n : min(max(int(ceilf(fmaf(tend - t0, inv_h, -0.5f))), 0), n);
     __syncthreads();  // previous chunk's samples are done with the box
-    // stage the box: one TMA bulk copy per row (warp 0), completion on the mbarrier
-    if (warp == 0) {
-      if (lane == 0) mbar_arrive_expect_tx(&box_bar, unsigned(rows * cols) * 16u);
-      __syncwarp();
-      for (int rr = lane; rr < rows; rr += 32)
-        tma_bulk_g2s(box_s + rr * pitch, src + int64_t(r0 + rr) * P + c0, unsigned(cols) * 16u, &box_bar);
+    if constexpr (LANE) {
+      // stage lane 0 of the box's texels: warp w takes rows w, w + 8, ...
+      float* box1 = reinterpret_cast<float*>(box_s);
+      for (int rr = warp; rr < rows; rr += kFwdThreads / 32) {
+        const float4* row = src + int64_t(r0 + rr) * P + c0;
+        for (int cc = lane; cc < cols; cc += 32) box1[rr * pitch + cc] = __ldg(row + cc).x;
+      }
+      __syncthreads();
+    } else {
+      // stage the box: one TMA bulk copy per row (warp 0), completion on the mbarrier
+      if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&box_bar, unsigned(rows * cols) * 16u);
+        __syncwarp();
+        for (int rr = lane; rr < rows; rr += 32)
+          tma_bulk_g2s(box_s + rr * pitch, src + int64_t(r0 + rr) * P + c0, unsigned(cols) * 16u, &box_bar);
+      }
+      mbar_wait(&box_bar, unsigned(c & 1));
     }
-    mbar_wait(&box_bar, unsigned(c & 1));
     const float ox = float(c0), oy = float(r0);
     const int jmax = cols - 2, imax = rows - 2;
     const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
@@ -240,16 +257,23 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
       const float fx = px - fj, fy = py - fi;
       const int j = min(max(int(fj), 0), jmax);
       const int i = min(max(int(fi), 0), imax);
-      const float4* q = box_s + (i * pitch + j + dA);
-      const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
       const float gx = 1.f - fx, gy = 1.f - fy;
       const float ya = rs ? fy : gy, yb = rs ? gy : fy;
       const float xa = cs ? fx : gx, xb = cs ? gx : fx;
       const float w1 = xa * ya, w2 = xb * ya, w3 = xa * yb, w4 = xb * yb;
+      if constexpr (LANE) {
+        const float* q = reinterpret_cast<const float*>(box_s) + (i * pitch + j + dA);
+        const float v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
+        a0 = fmaf(w1, v1, fmaf(w2, v2, fmaf(w3, v3, fmaf(w4, v4, a0))));
+        continue;
+      } else {
+      const float4* q = box_s + (i * pitch + j + dA);
+      const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
       a0 = fmaf(w1, v1.x, fmaf(w2, v2.x, fmaf(w3, v3.x, fmaf(w4, v4.x, a0))));
       a1 = fmaf(w1, v1.y, fmaf(w2, v2.y, fmaf(w3, v3.y, fmaf(w4, v4.y, a1))));
       a2 = fmaf(w1, v1.z, fmaf(w2, v2.z, fmaf(w3, v3.z, fmaf(w4, v4.z, a2))));
       a3 = fmaf(w1, v1.w, fmaf(w2, v2.w, fmaf(w3, v3.w, fmaf(w4, v4.w, a3))));
+      }
     }
   }
   if (!valid) return;
@@ -322,18 +346,28 @@ constexpr int kMaxBpChunk = 32;  // angles per staging pass (one constants recor
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 
-template <int KIND, class TOut>
-__global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backproject_kernel(
+// LANE (batch 1): only lane 0 of the packed group carries a sinogram; the
+// windows are staged as scalars (lane 0 of each cell) and the CTA has 512
+// threads x 2 pixels, so the 32x32 tiles of one image fill the GPU.  Per
+// pixel the operations on lane 0 and their order are the packed kernel's
+// (same tile-relative constants), so the results are bit-identical.
+template <int KIND, class TOut, bool LANE>
+__global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == kBpParallel ? 4 : 3))
+    backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
     int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
-  extern __shared__ float4 smem[];
+  using Cell = typename std::conditional<LANE, float, float4>::type;
+  constexpr int RPT = LANE ? 2 : kRowsPerThread;  // pixels (rows) per thread
+  constexpr int NT = kTile * kTile / RPT;         // threads
+  extern __shared__ float4 smem_raw[];
+  Cell* smem = reinterpret_cast<Cell*>(smem_raw);
   // this tile's staged cells per angle, and as many angles per pass as fit
   const int window = __ldg(tile_window + blockIdx.y * gridDim.x + blockIdx.x);
   const int chunk = min(kMaxBpChunk, cells / window);
-  float4* win = smem;                                                  // chunk * window <= cells
-  Const* cst = reinterpret_cast<Const*>(smem + cells);                 // kMaxBpChunk records
+  Cell* win = smem;                                                    // chunk * window <= cells
+  Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kMaxBpChunk records
   int* ws_s = reinterpret_cast<int*>(cst + kMaxBpChunk);               // kMaxBpChunk window starts
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kTile + tx;
@@ -347,9 +381,9 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
   const double y0 = half - double(i0) - 0.5;
   const float4* sg = sino + g * int64_t(na) * nd;
 
-  float4 acc[kRowsPerThread];
+  float4 acc[RPT];
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < RPT; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
 
   for (int a0 = 0; a0 < na; a0 += chunk) {
     const int nac = min(chunk, na - a0);
@@ -405,12 +439,15 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
     }
     __syncthreads();
     // ---- stage the detector windows (coalesced 16-byte cells)
-    for (int e = tid; e < nac * window; e += kBpThreads) {
+    for (int e = tid; e < nac * window; e += NT) {
       const int q = e / window, cidx = e - q * window;
       const int k = ws_s[q] + cidx;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k >= 0 && k < nd) v = __ldg(sg + int64_t(a0 + q) * nd + k);
-      win[e] = v;
+      if constexpr (LANE)
+        win[e] = v.x;
+      else
+        win[e] = v;
     }
     __syncthreads();
     // ---- accumulate
@@ -418,10 +455,10 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
     const float kmag_f = float(kmag);
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
-      const float4* w = win + q * window;
+      const Cell* w = win + q * window;
 #pragma unroll
-      for (int r = 0; r < kRowsPerThread; ++r) {
-        const float lx = float(tx), ly = float(ty + r * (kTile / kRowsPerThread));
+      for (int r = 0; r < RPT; ++r) {
+        const float lx = float(tx), ly = float(ty + r * (kTile / RPT));
         float kf;
         if constexpr (KIND == kBpParallel) {
           kf = fmaf(lx, k.cx, fmaf(ly, k.cy, k.base));
@@ -441,12 +478,17 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
         const float fk = floorf(kf);
         const float wt = kf - fk;
         const int c0 = min(max(int(fk), 0), window - 2);
-        const float4 s0 = w[c0], s1 = w[c0 + 1];
         const float wl = 1.f - wt;
-        acc[r].x = fmaf(wt, s1.x, fmaf(wl, s0.x, acc[r].x));
-        acc[r].y = fmaf(wt, s1.y, fmaf(wl, s0.y, acc[r].y));
-        acc[r].z = fmaf(wt, s1.z, fmaf(wl, s0.z, acc[r].z));
-        acc[r].w = fmaf(wt, s1.w, fmaf(wl, s0.w, acc[r].w));
+        if constexpr (LANE) {
+          const float s0 = w[c0], s1 = w[c0 + 1];
+          acc[r].x = fmaf(wt, s1, fmaf(wl, s0, acc[r].x));
+        } else {
+          const float4 s0 = w[c0], s1 = w[c0 + 1];
+          acc[r].x = fmaf(wt, s1.x, fmaf(wl, s0.x, acc[r].x));
+          acc[r].y = fmaf(wt, s1.y, fmaf(wl, s0.y, acc[r].y));
+          acc[r].z = fmaf(wt, s1.z, fmaf(wl, s0.z, acc[r].z));
+          acc[r].w = fmaf(wt, s1.w, fmaf(wl, s0.w, acc[r].w));
+        }
       }
     }
     __syncthreads();
@@ -454,8 +496,8 @@ __global__ void __launch_bounds__(kBpThreads, KIND == kBpParallel ? 4 : 3) backp
   // ---- store
   const int P = s + 2;
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
-    const int i = i0 + ty + r * (kTile / kRowsPerThread), j = j0 + tx;
+  for (int r = 0; r < RPT; ++r) {
+    const int i = i0 + ty + r * (kTile / RPT), j = j0 + tx;
     if (i >= s || j >= s) continue;
     if (epi.mode == kOutUser) {
       const float v[kPack] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
@@ -527,14 +569,24 @@ void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4
   RK_CUDA(cudaGetLastError());
 }
 
+// Batch 1: the single-lane kernels (RK_SINGLE_LANE=0 forces the packed ones, for A/B).
+static bool single_lane(int64_t batch) {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_SINGLE_LANE");
+    return !(e && e[0] == '0');
+  }();
+  return on && batch == 1;
+}
+
 void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
   const ForwardSchedule& F = p.fwd;
   dim3 grid(unsigned(F.cta.size()), unsigned(groups_of(batch)));
-  const size_t smem = size_t(F.max_box) * sizeof(float4);
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = forward_kernel<T>;
+    const bool lane = single_lane(batch);
+    auto kern = lane ? forward_kernel<T, true> : forward_kernel<T, false>;
+    const size_t smem = size_t(F.max_box) * (lane ? sizeof(float) : sizeof(float4));
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FORWARD, st);
     kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
@@ -549,14 +601,19 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                         cudaStream_t st, BpEpilogue epi) {
   const int tiles = int((p.s + kTile - 1) / kTile);
   dim3 grid(tiles, tiles, unsigned(groups_of(batch)));
-  dim3 block(kTile, kTile / kRowsPerThread);
+  const bool lane = single_lane(batch);
+  dim3 block(kTile, kTile / (lane ? 2 : kRowsPerThread));
   const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
   const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
   const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T>
-                                    : kind == kBpFan32 ? backproject_kernel<kBpFan32, T> : backproject_kernel<kBpFan64, T>;
+    auto kern = lane ? (kind == kBpParallel ? backproject_kernel<kBpParallel, T, true>
+                        : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, true>
+                                            : backproject_kernel<kBpFan64, T, true>)
+                     : (kind == kBpParallel ? backproject_kernel<kBpParallel, T, false>
+                        : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false>
+                                            : backproject_kernel<kBpFan64, T, false>);
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
