@@ -138,6 +138,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
       : "memory");
 }
 
+// cp.async (LDGSTS) helpers
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (lanes)
 
 // Ray-driven forward projection (projector.cpp:66-139), one CTA per block of
@@ -164,7 +172,8 @@ template <class TOut, bool LANE>
 __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
-    const int2* __restrict__ warps, int na, int nd, int64_t batch, TOut* __restrict__ sino, FwdEpilogue epi) {
+    const int2* __restrict__ warps, int na, int nd, int64_t batch, TOut* __restrict__ sino, FwdEpilogue epi,
+    int lane_box) {
   extern __shared__ float4 box_s[];
   __shared__ unsigned long long box_bar;  // TMA completion of the current chunk's box
   const int cta = blockIdx.x;
@@ -219,6 +228,22 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
   __syncthreads();
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   int m = 0;
+  // LANE: lane 0 of the box's texels by 4-byte cp.async (warp w takes rows w,
+  // w + 8, ...) into two alternating scalar boxes, the next chunk's copies in
+  // flight while the current chunk is marched
+  const int box_cells = lane_box;  // LANE: the second box's offset (max box cells of the plan)
+  auto stage_lane = [&](int cc_, float* dst) {
+    const int4 b = __ldg(bxs + cc_);
+    const int br0 = b.x & 0xffff, bc0 = b.x >> 16, brows = b.y & 0xffff, bcols = b.y >> 16, bpitch = b.z;
+    for (int rr = warp; rr < brows; rr += kFwdThreads / 32) {
+      const float4* row = src + int64_t(br0 + rr) * P + bc0;
+      for (int cc = lane; cc < bcols; cc += 32) cp_async4(dst + rr * bpitch + cc, row + cc);
+    }
+    cp_async_commit();
+  };
+  if constexpr (LANE) {
+    if (cfg.y > 0) stage_lane(0, reinterpret_cast<float*>(box_s));
+  }
   for (int c = 0; c < cfg.y; ++c) {
     const int4 bx = __ldg(bxs + c);  // CTA-uniform
     const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16, pitch = bx.z;
@@ -227,12 +252,13 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
     const int m_end =
         isinf(tend) ? n : min(max(int(ceilf(fmaf(tend - t0, inv_h, -0.5f))), 0), n);
     __syncthreads();  // previous chunk's samples are done with the box
+    const float* box1 = reinterpret_cast<const float*>(box_s) + (c & 1) * box_cells;
     if constexpr (LANE) {
-      // stage lane 0 of the box's texels: warp w takes rows w, w + 8, ...
-      float* box1 = reinterpret_cast<float*>(box_s);
-      for (int rr = warp; rr < rows; rr += kFwdThreads / 32) {
-        const float4* row = src + int64_t(r0 + rr) * P + c0;
-        for (int cc = lane; cc < cols; cc += 32) box1[rr * pitch + cc] = __ldg(row + cc).x;
+      if (c + 1 < cfg.y) {
+        stage_lane(c + 1, reinterpret_cast<float*>(box_s) + ((c + 1) & 1) * box_cells);
+        cp_async_wait_1();
+      } else {
+        cp_async_wait_all();
       }
       __syncthreads();
     } else {
@@ -262,7 +288,7 @@ __global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
       const float xa = cs ? fx : gx, xb = cs ? gx : fx;
       const float w1 = xa * ya, w2 = xb * ya, w3 = xa * yb, w4 = xb * yb;
       if constexpr (LANE) {
-        const float* q = reinterpret_cast<const float*>(box_s) + (i * pitch + j + dA);
+        const float* q = box1 + (i * pitch + j + dA);
         const float v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
         a0 = fmaf(w1, v1, fmaf(w2, v2, fmaf(w3, v3, fmaf(w4, v4, a0))));
         continue;
@@ -586,13 +612,13 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
     using T = decltype(tag);
     const bool lane = single_lane(batch);
     auto kern = lane ? forward_kernel<T, true> : forward_kernel<T, false>;
-    const size_t smem = size_t(F.max_box) * (lane ? sizeof(float) : sizeof(float4));
+    const size_t smem = size_t(F.max_box) * (lane ? 2 * sizeof(float) : sizeof(float4));
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FORWARD, st);
     kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
                                          p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int4>(),
                                          p.fwd_warps.as<int2>(), int(p.na), int(p.nd), batch,
-                                         static_cast<T*>(sino), epi);
+                                         static_cast<T*>(sino), epi, int(F.max_box));
   });
   RK_CUDA(cudaGetLastError());
 }
