@@ -323,8 +323,13 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     Shape sh;
     int64_t budget;
   };
-  const Tier tiers[] = {{{8, 1}, 4096},  {{4, 2}, 4096},  {{2, 4}, 4096},  {{1, 8}, 4096},  {{8, 1}, 12288},
-                        {{4, 2}, 12288}, {{4, 1}, 12288}, {{2, 1}, 12288}, {{1, 1}, 12288}};
+  // First choice: 54 KB boxes (four CTAs per SM); then 64 KB (three).
+  const char* be = std::getenv("RK_FWD_BOX");
+  const int64_t b0 = be ? std::max<int64_t>(512, std::atoll(be)) : F.box_budget;
+  const int64_t b1 = std::max<int64_t>(b0, 4096);
+  const Tier tiers[] = {{{8, 1}, b0},     {{8, 1}, b1},     {{4, 2}, b1},     {{2, 4}, b1},
+                        {{1, 8}, b1},     {{8, 1}, 12288}, {{4, 2}, 12288}, {{4, 1}, 12288},
+                        {{2, 1}, 12288}, {{1, 1}, 12288}};
   for (const Tier& tier : tiers) {
     const Shape sh = tier.sh;
     if (sh.db > 1 && nkb < sh.db && sh.db != 8) continue;

@@ -169,7 +169,7 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // and FMAs of the packed loop, with the same operations on lane 0 in the same
 // order, so its results equal the packed kernel's bit for bit.
 template <class TOut, bool LANE>
-__global__ void __launch_bounds__(kFwdThreads, 3) forward_kernel(
+__global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
     const int2* __restrict__ warps, int na, int nd, int64_t batch, TOut* __restrict__ sino, FwdEpilogue epi,

@@ -71,7 +71,7 @@ struct RayD {
 };
 
 struct ForwardSchedule {
-  int64_t box_budget = 4096;       // float4 cells per staged box (64 KB: three CTAs per SM)
+  int64_t box_budget = 3456;       // float4 cells per staged box (54 KB: four CTAs per SM)
   int shape_aa = 8, shape_db = 1;  // angles x 32-cell detector blocks per CTA
   int64_t max_box = 0;             // largest rows * pitch over all boxes (float4 cells)
   int64_t staged_texels = 0;       // per image group, all CTAs and chunks
