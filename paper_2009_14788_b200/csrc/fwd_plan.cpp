@@ -243,68 +243,69 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     double cost = 0.0, ideal = 0.0;  // simulated wavefronts: chosen layout, conflict-free
     std::vector<int4> boxes;
   };
+  // Layout (lane mapping, orientation, pitch, tap order) by simulation, then
+  // greedy chunks, for one CTA's 8 warps {angle, first cell}.
+  auto plan_cta = [&](const int2* wa, bool full8, CtaPlan& cp, std::vector<Pt>& sim) {
+    // Lane mappings (kernels.cu): a quarter warp covers 2^lq neighbouring
+    // angle slots x 8 >> lq neighbouring cells; lq = 0 (detector-major) is
+    // the only one for partial CTA shapes.  Near-parallel lines of one
+    // angle and short arcs of one cell's neighbouring angles conflict at
+    // different directions, so each CTA takes the cheapest.  Positions at
+    // a few aligned steps of the march, in lane order.
+    auto lane_ray = [&](int lq, int w, int l, int& a_out, int64_t& k_out) {
+      if (lq == 0) {
+        a_out = wa[w].x;
+        k_out = int64_t(wa[w].y) + l;
+        return;
+      }
+      const int t = w * 32 + l;
+      const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
+      const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
+      a_out = wa[(ag << lq) + aq].x;
+      k_out = int64_t(wa[0].y) + cg * (8 >> lq) + cq;
+    };
+    double best = 1e300;
+    for (int mapping = 0; mapping < (full8 ? 4 : 1); ++mapping) {
+      sim.clear();
+      for (int st = 0; st < 8; ++st) {
+        const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st) / 7.0);
+        for (int w = 0; w < 8; ++w)
+          for (int l = 0; l < 32; ++l) {
+            Pt q{NAN, NAN};
+            int a;
+            int64_t kk;
+            lane_ray(mapping, w, l, a, kk);
+            if (a >= 0 && kk < nd) {
+              const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
+              if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
+                const double m = std::floor((tt - ry.t0) / ry.h);
+                const double t = ry.t0 + (m + 0.5) * ry.h;
+                q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
+              }
+            }
+            sim.push_back(q);
+          }
+      }
+      for (int tr = 0; tr < 2; ++tr)
+        for (int swap = 0; swap < 3; ++swap)
+          for (int res = 0; res < 8; ++res) {
+            const double c = conflict_cost(sim, tr == 1, 64 + res, swap) *
+                             (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
+            if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap, cp.mapping = mapping;
+            if (mapping == 0 && tr == 0 && swap == 0 && res == 0) cp.ideal = ideal_cost(sim);
+          }
+    }
+    cp.cost = best;
+    cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
+  };
   auto plan_shape = [&](Shape sh, std::vector<CtaPlan>& plans) {
     std::vector<int2> warps = warps_of(sh);
     const int ctas = int(warps.size() / 8);
     plans.assign(size_t(ctas), CtaPlan{});
     auto work = [&](int lo, int hi) {
       std::vector<Pt> sim;
-      for (int cta = lo; cta < hi; ++cta) {
-        const int2* wa = &warps[size_t(cta) * 8];
-        CtaPlan& cp = plans[size_t(cta)];
-        // Lane mappings (kernels.cu): a quarter warp covers 2^lq neighbouring
-        // angle slots x 8 >> lq neighbouring cells; lq = 0 (detector-major) is
-        // the only one for partial CTA shapes.  Near-parallel lines of one
-        // angle and short arcs of one cell's neighbouring angles conflict at
-        // different directions, so each CTA takes the cheapest.  Positions at
-        // a few aligned steps of the march, in lane order.
-        const bool full8 = sh.aa == 8 && sh.db == 1;
-        auto lane_ray = [&](int lq, int w, int l, int& a_out, int64_t& k_out) {
-          if (lq == 0) {
-            a_out = wa[w].x;
-            k_out = int64_t(wa[w].y) + l;
-            return;
-          }
-          const int t = w * 32 + l;
-          const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
-          const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
-          a_out = wa[(ag << lq) + aq].x;
-          k_out = int64_t(wa[0].y) + cg * (8 >> lq) + cq;
-        };
-        double best = 1e300;
-        for (int mapping = 0; mapping < (full8 ? 4 : 1); ++mapping) {
-          sim.clear();
-          for (int st = 0; st < 8; ++st) {
-            const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st) / 7.0);
-            for (int w = 0; w < 8; ++w)
-              for (int l = 0; l < 32; ++l) {
-                Pt q{NAN, NAN};
-                int a;
-                int64_t kk;
-                lane_ray(mapping, w, l, a, kk);
-                if (a >= 0 && kk < nd) {
-                  const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
-                  if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
-                    const double m = std::floor((tt - ry.t0) / ry.h);
-                    const double t = ry.t0 + (m + 0.5) * ry.h;
-                    q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
-                  }
-                }
-                sim.push_back(q);
-              }
-          }
-          for (int tr = 0; tr < 2; ++tr)
-            for (int swap = 0; swap < 3; ++swap)
-              for (int res = 0; res < 8; ++res) {
-                const double c = conflict_cost(sim, tr == 1, 64 + res, swap) *
-                                 (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
-                if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap, cp.mapping = mapping;
-                if (mapping == 0 && tr == 0 && swap == 0 && res == 0) cp.ideal = ideal_cost(sim);
-              }
-        }
-        cp.cost = best;
-        cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
-      }
+      for (int cta = lo; cta < hi; ++cta)
+        plan_cta(&warps[size_t(cta) * 8], sh.aa == 8 && sh.db == 1, plans[size_t(cta)], sim);
     };
     const int nthreads = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), ctas));
     std::vector<std::thread> pool;
@@ -338,6 +339,42 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     std::vector<int2> warps = plan_shape(sh, plans);
     bool ok = true;
     for (const CtaPlan& cp : plans) ok &= cp.ok;
+    if (!ok && &tier == &tiers[0]) {
+      // Keep the small boxes (occupancy) for every CTA: a CTA whose shortest
+      // chunk overflows is replaced by CTAs marching halves of its angle
+      // slots (the other warps idle), recursively.
+      std::vector<int2> w2;
+      std::vector<CtaPlan> p2;
+      std::vector<Pt> sim;
+      ok = true;
+      std::function<void(const int2*, int, int)> split = [&](const int2* wa, int lo, int hi) {
+        int2 sub[8];
+        for (int w = 0; w < 8; ++w) sub[w] = (w >= lo && w < hi) ? wa[w] : make_int2(-1, wa[w].y);
+        CtaPlan cp;
+        plan_cta(sub, false, cp, sim);
+        if (cp.ok) {
+          w2.insert(w2.end(), sub, sub + 8);
+          p2.push_back(std::move(cp));
+        } else if (hi - lo > 1) {
+          split(wa, lo, (lo + hi) / 2);
+          split(wa, (lo + hi) / 2, hi);
+        } else {
+          ok = false;
+        }
+      };
+      for (size_t c = 0; c < plans.size() && ok; ++c) {
+        if (plans[c].ok) {
+          w2.insert(w2.end(), warps.begin() + int64_t(c) * 8, warps.begin() + int64_t(c + 1) * 8);
+          p2.push_back(std::move(plans[c]));
+        } else {
+          split(&warps[c * 8], 0, 8);
+        }
+      }
+      if (ok) {
+        warps = std::move(w2);
+        plans = std::move(p2);
+      }
+    }
     if (!ok) continue;
     F.shape_aa = sh.aa;
     F.shape_db = sh.db;
