@@ -337,13 +337,16 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
 // span / (sp (qy + D_so)).  kBpFan32 evaluates it relative to the tile corner,
 //   kf - ws = base + (dq K - u00 dd) / (den00 + dd),   dq, dd = O(tile) offsets,
 // which keeps fp32 accurate for moderate magnification; kBpFan64 (source close
-// to the image, plan.cpp picks it) runs the per-pixel map in fp64.
+// to the image, plan.cpp picks it) runs the per-pixel map in fp64.  With
+// dq = lx c - ly s and dd = -lx s - ly c both numerator and denominator are
+// affine in the tile offsets (lx, ly): num = A lx + B ly, den = den00 + C lx +
+// D ly (A, B from fp64), and every lx term is shared by a thread's pixels.
 enum { kBpParallel = 0, kBpFan32 = 1, kBpFan64 = 2 };
 struct ParConst {
   float base, cx, cy, pad;
 };
 struct Fan32Const {
-  float base, u00, den00, c, s, pad0, pad1, pad2;
+  float base, a, b, den00, c, d, pad0, pad1;
 };
 struct FanConst {
   double qx00, den00, c, s, offw, pad;
@@ -445,12 +448,14 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
         const double qx00 = x0 * c + y0 * sn;
         const double den00 = -x0 * sn + y0 * c + source_distance;
         if constexpr (KIND == kBpFan32) {
+          const double K = span / spacing, u00 = qx00 * K / den00;
           k.base = float(k00 - double(ws));
-          k.u00 = float(qx00 * (span / spacing) / den00);
+          k.a = float(c * K + u00 * sn);
+          k.b = float(u00 * c - sn * K);
           k.den00 = float(den00);
-          k.c = float(c);
-          k.s = float(sn);
-          k.pad0 = k.pad1 = k.pad2 = 0.f;
+          k.c = float(-sn);
+          k.d = float(-c);
+          k.pad0 = k.pad1 = 0.f;
         } else {
           k.qx00 = qx00;
           k.den00 = den00;
@@ -478,21 +483,29 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
     __syncthreads();
     // ---- accumulate
     const double kmag = span / spacing;
-    const float kmag_f = float(kmag);
+    const float lx = float(tx);
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
       const Cell* w = win + q * window;
+      // the pixel's column terms, shared by the thread's pixels (same value in
+      // the packed and single-lane kernels: only lx enters)
+      float col0 = 0.f, col1 = 0.f;
+      if constexpr (KIND == kBpParallel) {
+        col0 = fmaf(lx, k.cx, k.base);
+      } else if constexpr (KIND == kBpFan32) {
+        col0 = k.a * lx;
+        col1 = fmaf(k.c, lx, k.den00);
+      }
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const float lx = float(tx), ly = float(ty + r * (kTile / RPT));
+        const float ly = float(ty + r * (kTile / RPT));
         float kf;
         if constexpr (KIND == kBpParallel) {
-          kf = fmaf(lx, k.cx, fmaf(ly, k.cy, k.base));
+          kf = fmaf(ly, k.cy, col0);
         } else if constexpr (KIND == kBpFan32) {
-          const float dq = fmaf(lx, k.c, -ly * k.s);   // qx - qx00
-          const float dd = fmaf(-lx, k.s, -ly * k.c);  // den - den00
-          const float num = fmaf(dq, kmag_f, -k.u00 * dd);
-          kf = fmaf(num, rcp_approx(k.den00 + dd), k.base);
+          const float num = fmaf(k.b, ly, col0);  // (qx - qx00) K - u00 (den - den00)
+          const float den = fmaf(k.d, ly, col1);  // qy + D_so
+          kf = fmaf(num, rcp_approx(den), k.base);
         } else {
           const double dlx = double(lx), dly = double(ly);
           const double qx = fma(dlx, k.c, fma(-dly, k.s, k.qx00));
