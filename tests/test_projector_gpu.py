@@ -159,6 +159,29 @@ def test_batched_equals_per_element_bitwise(rk, oracle, cuda):
             assert torch.equal(bb[e:e + 1], rk.backprojection(g, fe))
 
 
+@pytest.mark.parametrize("name,mk", [
+    ("par-160-120", lambda rk: par(rk, 160, 120)),
+    ("par-96-70-det131-sp0.8", lambda rk: par(rk, 96, 70, 131, 0.8)),
+    ("fan-128-100-D200", lambda rk: fan(rk, 128, 100, 200.0)),
+    ("fan-96-64-D70-fp64map", lambda rk: fan(rk, 96, 64, 70.0, det_distance=300.0)),
+])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16])
+def test_single_lane_equals_packed_bitwise(rk, oracle, cuda, name, mk, dtype):
+    """Batch 1 runs the single-lane kernels (kernels.cu, LANE); they must equal
+    the packed kernels' lane results bit for bit (acceptance.cpp:340-389, C9)."""
+    g = mk(rk)
+    B = 6
+    imgs = batched_phantom(oracle, g.image_size, B)
+    imgs[3] = oracle.rng_uniform(7, g.image_size ** 2).reshape(g.image_size, g.image_size)
+    x = dev(imgs, cuda).to(dtype)
+    fb = rk.forward(g, x)
+    bb = rk.backprojection(g, fb)
+    for e in (0, 3, 5):
+        fe = rk.forward(g, x[e:e + 1])
+        assert torch.equal(fb[e:e + 1], fe)
+        assert torch.equal(bb[e:e + 1], rk.backprojection(g, fe))
+
+
 def test_quadrature_step(rk, oracle, cuda):
     """test_projector.cpp:268-279 + oracle parity at step 0.5."""
     img = oracle.shepp_logan(32, np.float64)
