@@ -132,9 +132,23 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
     p.pipe_in[i].reserve(size_t(chunk) * in_item);
     p.pipe_out[i].reserve(size_t(chunk) * out_item);
   }
+  // chunk sizes: ramp up from one packed group and back down at the end, so
+  // the copy-in before the first kernel and the copy-out after the last one
+  // (the parts no kernel overlaps) are short
+  std::vector<int64_t> sizes, ramp;
+  for (int64_t c = rk::kPack; c < chunk; c *= 2) ramp.push_back(c);
+  int64_t ramp_total = 0;
+  for (int64_t c : ramp) ramp_total += 2 * c;
+  if (!ramp.empty() && batch >= ramp_total + chunk) {
+    sizes = ramp;
+    for (int64_t rem = batch - ramp_total; rem > 0; rem -= std::min(chunk, rem)) sizes.push_back(std::min(chunk, rem));
+    sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
+  } else {
+    for (int64_t rem = batch; rem > 0; rem -= std::min(chunk, rem)) sizes.push_back(std::min(chunk, rem));
+  }
   int slot = 0;
-  for (int64_t b0 = 0; b0 < batch; b0 += chunk, slot ^= 1) {
-    const int64_t nb = std::min(chunk, batch - b0);
+  int64_t b0 = 0;
+  for (const int64_t nb : sizes) {
     cudaStream_t st = p.copy_streams[slot];
     const char* src = static_cast<const char*>(h_in) + size_t(b0) * in_item;
     char* dst = static_cast<char*>(h_out) + size_t(b0) * out_item;
@@ -142,6 +156,8 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
     body(p.pipe_in[slot].ptr, nb, p.pipe_out[slot].ptr, slot, st);
     RK_CUDA(cudaMemcpyAsync(dst, p.pipe_out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
     if (!pinned_in || !pinned_out) RK_CUDA(cudaStreamSynchronize(st));
+    b0 += nb;
+    slot ^= 1;
   }
   for (auto s : p.copy_streams) RK_CUDA(cudaStreamSynchronize(s));
 }
