@@ -12,7 +12,7 @@ import os
 from .errors import CudaError, NumericalError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libradon_b200.so")
+LIB_PATH = os.environ.get("RK_LIB") or os.path.join(_HERE, "libradon_b200.so")  # RK_LIB: A/B builds
 
 RK_OK, RK_ERR_VALIDATION, RK_ERR_NUMERICAL, RK_ERR_CUDA = 0, 1, 2, 3
 RK_F16, RK_F32, RK_F64 = 0, 1, 2
