@@ -4,11 +4,12 @@
 // :106-123).
 //
 // One CTA filters the four rows (b = 4g..4g+3, angle a) that share one
-// packed float4 sinogram cell, as two complex shared-memory radix-2 FFTs:
-// the response is real and even, so for z = x + i y,
-// IFFT(FFT(z) H) = x*h + i (y*h) filters two real rows at once (SURVEY
-// 7.3-6).  The inverse transform reuses the forward twiddles through
-// IFFT(X) = conj(FFT(conj(X))) / P.
+// packed float4 sinogram cell, as two complex shared-memory FFTs: the
+// response is real and even, so for z = x + i y, IFFT(FFT(z) H) = x*h + i (y*h)
+// filters two real rows at once.  The forward transform is
+// decimation-in-frequency (natural in, bit-reversed out), the response is
+// applied in bit-reversed order, and the inverse is decimation-in-time with
+// conjugate twiddles (bit-reversed in, natural out): no permutation pass.
 #include <cuda_fp16.h>
 
 #include "rk_internal.hpp"
@@ -41,23 +42,78 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// In-place radix-2 DIT over bit-reversed input, two independent signals.
-__device__ void fft2_inplace(float2* za, float2* zb, int P, const float2* __restrict__ tw) {
-  for (int len = 2; len <= P; len <<= 1) {
-    const int half = len >> 1, stride = P / len;
-    for (int bidx = threadIdx.x; bidx < P / 2; bidx += blockDim.x) {
-      const int grp = bidx / half, k = bidx - grp * half;
-      const int i = grp * len + k;
-      const float2 w = __ldg(tw + k * stride);
-      const float2 ua = za[i], va = cmul(za[i + half], w);
-      za[i] = make_float2(ua.x + va.x, ua.y + va.y);
-      za[i + half] = make_float2(ua.x - va.x, ua.y - va.y);
-      const float2 ub = zb[i], vb = cmul(zb[i + half], w);
-      zb[i] = make_float2(ub.x + vb.x, ub.y + vb.y);
-      zb[i + half] = make_float2(ub.x - vb.x, ub.y - vb.y);
+// Shared-memory slot of complex element i: an XOR swizzle inside each block of
+// 16 (128 bytes) that makes every access pattern of the fused passes below
+// bank-conflict free (64-bit loads, half warps).
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 3) & 15); }
+
+__device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+
+// R consecutive radix-2 stages of an in-place FFT of 2^logn points fused in
+// registers: the group of element i0 holds i0 + m 2^lh (m < 2^R), so stages
+// lh+1 .. lh+R pair elements inside the group.  DIF (natural in, bit-reversed
+// out, W = exp(-2 pi i/n)): u + v, (u - v) W; DIT (bit-reversed in, natural
+// out): u + v W, u - v W, with conj(W) when CONJ (the unnormalised inverse).
+// Each butterfly is the radix-2 one with the stage's table twiddle; a
+// transform is ceil(logn / 3) shared-memory passes and barriers.  Two signals
+// (z, z + stride).
+template <int R, bool DIF, bool CONJ>
+__device__ __forceinline__ void fft_pass(float2* z, int stride, int logn, int lh, const float2* __restrict__ tw) {
+  const int gl = logn - R;  // log2(groups per signal)
+  for (int t = threadIdx.x; t < (2 << gl); t += blockDim.x) {
+    const int sig = t >> gl, g = t & ((1 << gl) - 1);
+    const int lo = g & ((1 << lh) - 1), hi = g >> lh;
+    const int i0 = lo + (hi << (lh + R));
+    float2* a = z + sig * stride;
+    float2 x[1 << R];
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m) x[m] = a[swz(i0 + (m << lh))];
+#pragma unroll
+    for (int l = 0; l < R; ++l) {
+      const int bit = DIF ? R - 1 - l : l;  // partner bit of m in this layer
+#pragma unroll
+      for (int m = 0; m < (1 << R); ++m) {
+        if (m & (1 << bit)) continue;
+        const int q = m | (1 << bit);
+        const int k = lo + ((m & ((1 << bit) - 1)) << lh);
+        const float2 w = __ldg(tw + (k << (logn - lh - 1 - bit)));
+        const float2 u = x[m];
+        if (DIF) {
+          const float2 v = x[q];
+          x[m] = make_float2(u.x + v.x, u.y + v.y);
+          x[q] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
+        } else {
+          const float2 v = CONJ ? cmul_conj(x[q], w) : cmul(x[q], w);
+          x[m] = make_float2(u.x + v.x, u.y + v.y);
+          x[q] = make_float2(u.x - v.x, u.y - v.y);
+        }
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m) a[swz(i0 + (m << lh))] = x[m];
   }
+  __syncthreads();
+}
+
+// forward: natural -> bit-reversed (the short pass first, at the widest stride)
+__device__ void fft_dif(float2* z, int stride, int logn, const float2* __restrict__ tw) {
+  int lh = logn - logn % 3;
+  if (logn % 3 == 2) fft_pass<2, true, false>(z, stride, logn, lh, tw);
+  if (logn % 3 == 1) fft_pass<1, true, false>(z, stride, logn, lh, tw);
+  while (lh >= 3) {
+    lh -= 3;
+    fft_pass<3, true, false>(z, stride, logn, lh, tw);
+  }
+}
+
+// unnormalised inverse: bit-reversed -> natural
+__device__ void ifft_dit(float2* z, int stride, int logn, const float2* __restrict__ tw) {
+  int lh = 0;
+  for (; lh + 3 <= logn; lh += 3) fft_pass<3, false, true>(z, stride, logn, lh, tw);
+  if (logn - lh == 2) fft_pass<2, false, true>(z, stride, logn, lh, tw);
+  if (logn - lh == 1) fft_pass<1, false, true>(z, stride, logn, lh, tw);
 }
 
 template <class TIn, class TOut, bool PACKED>
@@ -67,12 +123,12 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
                                                                 const float2* __restrict__ tw, float scale,
                                                                 TOut* __restrict__ out, float4* __restrict__ packed) {
   extern __shared__ float2 fsm[];
-  float2* za = fsm;      // rows q=0 (re) and q=1 (im)
+  float2* za = fsm;      // rows q=0 (re) and q=1 (im), swizzled slots (swz)
   float2* zb = fsm + P;  // rows q=2 (re) and q=3 (im)
   const int a = blockIdx.x;
   const int64_t g = blockIdx.y;
   const int shift = 32 - logP;
-  // ---- load (zero pad) into bit-reversed positions
+  // ---- load (zero pad), natural order
   const TIn* rows[4];
   bool valid[4];
 #pragma unroll
@@ -88,39 +144,27 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
       for (int q = 0; q < 4; ++q)
         if (valid[q]) v[q] = ld_f32(rows[q] + k);
     }
-    const int rk = int(__brev(unsigned(k)) >> shift);
-    za[rk] = make_float2(v[0], v[1]);
-    zb[rk] = make_float2(v[2], v[3]);
+    za[swz(k)] = make_float2(v[0], v[1]);
+    zb[swz(k)] = make_float2(v[2], v[3]);
   }
   __syncthreads();
-  fft2_inplace(za, zb, P, tw);
-  // ---- multiply by the real, even response and conjugate (inverse via forward FFT)
+  fft_dif(fsm, P, logP, tw);
+  // ---- multiply by the real, even response; slot q holds frequency brev(q)
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
-    const float h = __ldg(resp + (q <= P / 2 ? q : P - q));
-    const float2 x = za[q], y = zb[q];
-    za[q] = make_float2(x.x * h, -(x.y * h));
-    zb[q] = make_float2(y.x * h, -(y.y * h));
+    const int f = int(__brev(unsigned(q)) >> shift);
+    const float h = __ldg(resp + (f <= P / 2 ? f : P - f));
+    const int sq = swz(q);
+    const float2 x = za[sq], y = zb[sq];
+    za[sq] = make_float2(x.x * h, x.y * h);
+    zb[sq] = make_float2(y.x * h, y.y * h);
   }
   __syncthreads();
-  // ---- bit-reversal permutation in place
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    const int rk = int(__brev(unsigned(k)) >> shift);
-    if (k < rk) {
-      float2 t = za[k];
-      za[k] = za[rk];
-      za[rk] = t;
-      t = zb[k];
-      zb[k] = zb[rk];
-      zb[rk] = t;
-    }
-  }
-  __syncthreads();
-  fft2_inplace(za, zb, P, tw);
+  ifft_dit(fsm, P, logP, tw);
   // ---- crop, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
   const float inv = 1.0f / float(P);
   for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    const float2 x = za[k], y = zb[k];
-    const float v[4] = {(x.x * inv) * scale, (-x.y * inv) * scale, (y.x * inv) * scale, (-y.y * inv) * scale};
+    const float2 x = za[swz(k)], y = zb[swz(k)];
+    const float v[4] = {(x.x * inv) * scale, (x.y * inv) * scale, (y.x * inv) * scale, (y.y * inv) * scale};
     if (PACKED) {
       // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows
       // to the storage precision first (sino_filter.cpp:123, 126-128)
