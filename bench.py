@@ -460,7 +460,8 @@ def measure_extras(rk, _lib, dev):
     opa = rk.projector_operator(ga)
     for b in (1, 8):
         ya = rk.forward(ga, x[:b])
-        rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=1))  # warm-up (plans, scratch)
+        # warm-up: plans, scratch and GPU clocks (a short run leaves the clocks ramping into the timed one)
+        rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=20, inner_cg_iterations=50))
         ms = timed(lambda: rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=50,
                                                                              inner_cg_iterations=50)), runs=1)
         out[f"next_admm512_limited100_na512_b{b}_fp32"] = {"metric": "ADMM seconds per image (50 outer x 50 inner)",

@@ -12,6 +12,7 @@
 // conjugate twiddles (bit-reversed in, natural out): no permutation pass.
 #include <cuda_fp16.h>
 
+#include "fft_smem.cuh"
 #include "rk_internal.hpp"
 
 namespace rk {
@@ -37,84 +38,6 @@ template <>
 __device__ __forceinline__ double st_cast<double>(float v) { return double(v); }
 
 constexpr int kFilterThreads = 256;
-
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-
-// Shared-memory slot of complex element i: an XOR swizzle inside each block of
-// 16 (128 bytes) that makes every access pattern of the fused passes below
-// bank-conflict free (64-bit loads, half warps).
-__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 3) & 15); }
-
-__device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
-}
-
-// R consecutive radix-2 stages of an in-place FFT of 2^logn points fused in
-// registers: the group of element i0 holds i0 + m 2^lh (m < 2^R), so stages
-// lh+1 .. lh+R pair elements inside the group.  DIF (natural in, bit-reversed
-// out, W = exp(-2 pi i/n)): u + v, (u - v) W; DIT (bit-reversed in, natural
-// out): u + v W, u - v W, with conj(W) when CONJ (the unnormalised inverse).
-// Each butterfly is the radix-2 one with the stage's table twiddle; a
-// transform is ceil(logn / 3) shared-memory passes and barriers.  Two signals
-// (z, z + stride).
-template <int R, bool DIF, bool CONJ>
-__device__ __forceinline__ void fft_pass(float2* z, int stride, int logn, int lh, const float2* __restrict__ tw) {
-  const int gl = logn - R;  // log2(groups per signal)
-  for (int t = threadIdx.x; t < (2 << gl); t += blockDim.x) {
-    const int sig = t >> gl, g = t & ((1 << gl) - 1);
-    const int lo = g & ((1 << lh) - 1), hi = g >> lh;
-    const int i0 = lo + (hi << (lh + R));
-    float2* a = z + sig * stride;
-    float2 x[1 << R];
-#pragma unroll
-    for (int m = 0; m < (1 << R); ++m) x[m] = a[swz(i0 + (m << lh))];
-#pragma unroll
-    for (int l = 0; l < R; ++l) {
-      const int bit = DIF ? R - 1 - l : l;  // partner bit of m in this layer
-#pragma unroll
-      for (int m = 0; m < (1 << R); ++m) {
-        if (m & (1 << bit)) continue;
-        const int q = m | (1 << bit);
-        const int k = lo + ((m & ((1 << bit) - 1)) << lh);
-        const float2 w = __ldg(tw + (k << (logn - lh - 1 - bit)));
-        const float2 u = x[m];
-        if (DIF) {
-          const float2 v = x[q];
-          x[m] = make_float2(u.x + v.x, u.y + v.y);
-          x[q] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
-        } else {
-          const float2 v = CONJ ? cmul_conj(x[q], w) : cmul(x[q], w);
-          x[m] = make_float2(u.x + v.x, u.y + v.y);
-          x[q] = make_float2(u.x - v.x, u.y - v.y);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < (1 << R); ++m) a[swz(i0 + (m << lh))] = x[m];
-  }
-  __syncthreads();
-}
-
-// forward: natural -> bit-reversed (the short pass first, at the widest stride)
-__device__ void fft_dif(float2* z, int stride, int logn, const float2* __restrict__ tw) {
-  int lh = logn - logn % 3;
-  if (logn % 3 == 2) fft_pass<2, true, false>(z, stride, logn, lh, tw);
-  if (logn % 3 == 1) fft_pass<1, true, false>(z, stride, logn, lh, tw);
-  while (lh >= 3) {
-    lh -= 3;
-    fft_pass<3, true, false>(z, stride, logn, lh, tw);
-  }
-}
-
-// unnormalised inverse: bit-reversed -> natural
-__device__ void ifft_dit(float2* z, int stride, int logn, const float2* __restrict__ tw) {
-  int lh = 0;
-  for (; lh + 3 <= logn; lh += 3) fft_pass<3, false, true>(z, stride, logn, lh, tw);
-  if (logn - lh == 2) fft_pass<2, false, true>(z, stride, logn, lh, tw);
-  if (logn - lh == 1) fft_pass<1, false, true>(z, stride, logn, lh, tw);
-}
 
 template <class TIn, class TOut, bool PACKED>
 __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
@@ -144,26 +67,26 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
       for (int q = 0; q < 4; ++q)
         if (valid[q]) v[q] = ld_f32(rows[q] + k);
     }
-    za[swz(k)] = make_float2(v[0], v[1]);
-    zb[swz(k)] = make_float2(v[2], v[3]);
+    za[fft_swz(k)] = make_float2(v[0], v[1]);
+    zb[fft_swz(k)] = make_float2(v[2], v[3]);
   }
   __syncthreads();
-  fft_dif(fsm, P, logP, tw);
+  fft_dif_seq(fsm, 2, P, logP, tw);
   // ---- multiply by the real, even response; slot q holds frequency brev(q)
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     const int f = int(__brev(unsigned(q)) >> shift);
     const float h = __ldg(resp + (f <= P / 2 ? f : P - f));
-    const int sq = swz(q);
+    const int sq = fft_swz(q);
     const float2 x = za[sq], y = zb[sq];
     za[sq] = make_float2(x.x * h, x.y * h);
     zb[sq] = make_float2(y.x * h, y.y * h);
   }
   __syncthreads();
-  ifft_dit(fsm, P, logP, tw);
+  ifft_dit_seq(fsm, 2, P, logP, tw);
   // ---- crop, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
   const float inv = 1.0f / float(P);
   for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    const float2 x = za[swz(k)], y = zb[swz(k)];
+    const float2 x = za[fft_swz(k)], y = zb[fft_swz(k)];
     const float v[4] = {(x.x * inv) * scale, (x.y * inv) * scale, (y.x * inv) * scale, (y.y * inv) * scale};
     if (PACKED) {
       // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows

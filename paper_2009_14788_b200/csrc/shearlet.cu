@@ -7,8 +7,9 @@
 //
 // Layout and passes (no transposes, no bit-reversal permutes):
 //   * 2-D FFTs are a row pass and a column pass over natural [row][col]
-//     planes, each a shared-memory radix-2 FFT of a CTA tile (rows, or a
-//     tile of adjacent columns read with coalesced row segments).
+//     planes, each a shared-memory FFT of a CTA tile (rows, or a tile of
+//     adjacent columns read with coalesced row segments) with three radix-2
+//     stages fused per register pass (fft_smem.cuh).
 //   * Forward transforms are decimation-in-frequency (natural in, bit-reversed
 //     out) and inverse ones decimation-in-time (bit-reversed in, natural out),
 //     so spectra live in bit-reversed (row, col) order and the multipliers are
@@ -28,6 +29,7 @@
 // non-finite flag), and synthesis can read (z1 - u1) instead of c.
 #include <cuda_fp16.h>
 
+#include "fft_smem.cuh"
 #include "rk_internal.hpp"
 
 namespace rk {
@@ -75,47 +77,13 @@ constexpr int kTileMin = 4096;  // complex elements per CTA tile (>= one row, <=
 constexpr int kPerThread = 16;  // tile elements per thread
 constexpr int kPairChunk = 8;   // coefficient pairs per synthesis accumulation (fixed: batch-independent order)
 
+// shared-memory slot of tile element e (row e >> logn of the tile, swizzled within the row)
+__device__ __forceinline__ int srow(int e, int logn) {
+  return ((e >> logn) << logn) | fft_swz(e & ((1 << logn) - 1));
+}
+
 // tile elements for an n x n plane: kTileMin, at least one row, at most the plane
 __host__ __device__ inline int tile_of(int n) { return min(max(kTileMin, n), n * n); }
-
-// cnt sequences of n = 2^logn complex values at stride ld.  DIF forward:
-// natural in, bit-reversed out, W = exp(-2 pi i / n).
-template <class C>
-__device__ void fft_dif(C* a, int cnt, int logn, int ld, const C* __restrict__ tw) {
-  const int halfn = 1 << (logn - 1);
-  const int tid = threadIdx.x, nt = blockDim.x, total = cnt * halfn;
-  for (int s = logn; s >= 1; --s) {
-    const int half = 1 << (s - 1), tsh = logn - s;
-    for (int b = tid; b < total; b += nt) {
-      const int r = b >> (logn - 1), bb = b & (halfn - 1);
-      const int k = bb & (half - 1), i = ((bb >> (s - 1)) << s) + k;
-      C* row = a + r * ld;
-      const C u = row[i], v = row[i + half];
-      row[i] = {u.x + v.x, u.y + v.y};
-      row[i + half] = cmul(C{u.x - v.x, u.y - v.y}, tw[k << tsh]);
-    }
-    __syncthreads();
-  }
-}
-
-// DIT inverse (unnormalised): bit-reversed in, natural out, W = exp(+2 pi i / n).
-template <class C>
-__device__ void ifft_dit(C* a, int cnt, int logn, int ld, const C* __restrict__ tw) {
-  const int halfn = 1 << (logn - 1);
-  const int tid = threadIdx.x, nt = blockDim.x, total = cnt * halfn;
-  for (int s = 1; s <= logn; ++s) {
-    const int half = 1 << (s - 1), tsh = logn - s;
-    for (int b = tid; b < total; b += nt) {
-      const int r = b >> (logn - 1), bb = b & (halfn - 1);
-      const int k = bb & (half - 1), i = ((bb >> (s - 1)) << s) + k;
-      C* row = a + r * ld;
-      const C u = row[i], v = cmul_conj(row[i + half], tw[k << tsh]);
-      row[i] = {u.x + v.x, u.y + v.y};
-      row[i + half] = {u.x - v.x, u.y - v.y};
-    }
-    __syncthreads();
-  }
-}
 
 // ADMM analysis epilogue (admm.cpp:150-153), fp32 like the reference's float path
 struct AdmmStore {
@@ -189,12 +157,12 @@ __global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src,
       im = ld_r<R>(in1 + base + e);
       if (s1) im = im - ld_r<R>(s1 + base + e);
     }
-    sm[e] = {re, im};
+    sm[srow(e, logn)] = {re, im};
   }
   __syncthreads();
-  fft_dif(sm, nr, logn, n, tw);
+  fft_dif_seq(sm, nr, n, logn, tw);
   C* o = out + p * plane + base;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) o[e] = sm[e];
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) o[e] = sm[srow(e, logn)];
 }
 
 // inverse row DIT of complex rows, scaled: Re -> out0, Im -> out1 (when present)
@@ -219,9 +187,9 @@ __global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* _
   const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
   const int64_t base = lr0 * n;
   const C* src = in + p * plane + base;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = src[e];
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[srow(e, logn)] = src[e];
   __syncthreads();
-  ifft_dit(sm, nr, logn, n, tw);
+  ifft_dit_seq(sm, nr, n, logn, tw);
   int64_t o0, o1 = -1;  // element offsets of the two output planes
   int k0 = 0;
   if (m.map == 0) {
@@ -233,7 +201,7 @@ __global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* _
     if (k0 + 1 < m.K) o1 = o0 + plane;
   }
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-    const C v = sm[e];
+    const C v = sm[srow(e, logn)];
     const R re = v.x * scale, im = v.y * scale;
     if (admm.z1 == nullptr) {
       dst[o0 + base + e] = st_r<T>(re);
@@ -254,20 +222,21 @@ template <class C>
 __device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int n, int tc, int c0, int ld) {
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
-    sm[c * ld + r] = src[int64_t(r) * n + c0 + c];
+    sm[c * ld + fft_swz(r)] = src[int64_t(r) * n + c0 + c];
   }
 }
 template <class C>
 __device__ __forceinline__ void store_cols(C* __restrict__ dst, const C* sm, int n, int tc, int c0, int ld) {
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
-    dst[int64_t(r) * n + c0 + c] = sm[c * ld + r];
+    dst[int64_t(r) * n + c0 + c] = sm[c * ld + fft_swz(r)];
   }
 }
 
 // mode 0: out = colDIF(in)                          (plane p -> p)
 // mode 1: out = colDIT^-1(in[b] * (M_2j + i M_2j+1)) (analysis item q = q0 + p: j = q / B, b = q % B)
 // mode 2: out = colDIT^-1(in)                       (plane p -> p)
+// mode 3: out = colDIT^-1(sum_c in[p][c])             (B = chunk partials per plane, summed in order)
 template <class R>
 __global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __restrict__ in, int mode, int logn,
                                                    const typename Cx<R>::T* __restrict__ tw,
@@ -289,28 +258,43 @@ __global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __res
     for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
       const int r = e / tc, c = e - r * tc;
       const int64_t gi = int64_t(r) * n + c0 + c;
-      sm[c * ld + r] = cmul(src[gi], mk[gi]);
+      sm[c * ld + fft_swz(r)] = cmul(src[gi], mk[gi]);
+    }
+  } else if (mode == 3) {
+    for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
+      const int r = e / tc, c = e - r * tc;
+      const int64_t gi = int64_t(r) * n + c0 + c;
+      C a = {R(0), R(0)};
+      for (int64_t k = 0; k < B; ++k) {
+        const C v = in[(p * B + k) * plane + gi];
+        a = {a.x + v.x, a.y + v.y};
+      }
+      sm[c * ld + fft_swz(r)] = a;
     }
   } else {
     load_cols(sm, in + p * plane, n, tc, c0, ld);
   }
   __syncthreads();
   if (mode == 0)
-    fft_dif(sm, tc, logn, ld, tw);
+    fft_dif_seq(sm, tc, ld, logn, tw);
   else
-    ifft_dit(sm, tc, logn, ld, tw);
+    ifft_dit_seq(sm, tc, ld, logn, tw);
   store_cols(out + p * plane, sm, n, tc, c0, ld);
 }
 
-// synthesis accumulation: for image b and a column tile, over the chunk's
-// pairs jj in ascending order: acc += colDIF(W[b][jj]) * (M_2j - i M_2j+1);
-// then S[b] += acc.  Each thread owns the same kPerThread tile elements
-// throughout, so the sum order per bin is fixed.
+// synthesis accumulation: for image b, a column tile and a chunk c of
+// kPairChunk coefficient pairs, over the chunk's pairs in ascending order:
+// acc += colDIF(W[b][pair]) * (M_2j - i M_2j+1); the chunk's sum goes to its
+// own partial plane Sp[b][c] (the final column pass adds the partials in
+// chunk order).  Each thread owns the same kPerThread tile elements
+// throughout, so the sum order per bin is fixed and batch-independent.
+// W holds the wave's pairs p0 .. p0 + np - 1 of every image (b * np + pair - p0).
 template <class R>
-__global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* __restrict__ W, int64_t J, int64_t j0,
-                                                       int logn, const typename Cx<R>::T* __restrict__ tw,
+__global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* __restrict__ W, int64_t np, int64_t p0,
+                                                       int64_t P, int64_t c0, int64_t ncw, int64_t nch, int logn,
+                                                       const typename Cx<R>::T* __restrict__ tw,
                                                        const typename Cx<R>::T* __restrict__ mult2,
-                                                       typename Cx<R>::T* __restrict__ S) {
+                                                       typename Cx<R>::T* __restrict__ Sp) {
   using C = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* sm = reinterpret_cast<C*>(smraw);
@@ -318,35 +302,36 @@ __global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* _
   const int64_t plane = int64_t(n) * n;
   const int tile = tile_of(n), tc = tile / n;
   const int tiles = n / tc;
-  const int64_t b = blockIdx.x / tiles;
-  const int c0 = int(blockIdx.x - b * tiles) * tc;
+  const int64_t cw = blockIdx.x % ncw, bt = blockIdx.x / ncw;
+  const int64_t b = bt / tiles;
+  const int c0t = int(bt - b * tiles) * tc;
+  const int64_t chunk = c0 + cw;
+  const int64_t ja = chunk * kPairChunk, jb = min(ja + kPairChunk, P);
   C acc[kPerThread];
 #pragma unroll
   for (int m = 0; m < kPerThread; ++m) acc[m] = {R(0), R(0)};
-  for (int64_t jj = 0; jj < J; ++jj) {
-    load_cols(sm, W + (b * J + jj) * plane, n, tc, c0, ld);
+  for (int64_t j = ja; j < jb; ++j) {
+    load_cols(sm, W + (b * np + (j - p0)) * plane, n, tc, c0t, ld);
     __syncthreads();
-    fft_dif(sm, tc, logn, ld, tw);
-    const C* mk = mult2 + (j0 + jj) * plane;
+    fft_dif_seq(sm, tc, ld, logn, tw);
+    const C* mk = mult2 + j * plane;
 #pragma unroll
     for (int m = 0; m < kPerThread; ++m) {
       const int e = threadIdx.x + m * blockDim.x;
       if (e >= tile) break;
       const int r = e / tc, c = e - r * tc;
-      const C v = cmul_conj(sm[c * ld + r], mk[int64_t(r) * n + c0 + c]);
+      const C v = cmul_conj(sm[c * ld + fft_swz(r)], mk[int64_t(r) * n + c0t + c]);
       acc[m] = {acc[m].x + v.x, acc[m].y + v.y};
     }
     __syncthreads();
   }
-  C* s = S + b * plane;
+  C* s = Sp + (b * nch + chunk) * plane;
 #pragma unroll
   for (int m = 0; m < kPerThread; ++m) {
     const int e = threadIdx.x + m * blockDim.x;
     if (e >= tile) break;
     const int r = e / tc, c = e - r * tc;
-    const int64_t gi = int64_t(r) * n + c0 + c;
-    const C a = s[gi];
-    s[gi] = {a.x + acc[m].x, a.y + acc[m].y};
+    s[int64_t(r) * n + c0t + c] = acc[m];
   }
 }
 
@@ -501,23 +486,27 @@ void backward_impl(Shearlet& sp, const T* coeff, const T* sub, int64_t batch, T*
   const int64_t plane = int64_t(n) * n, K = sp.n_coeff, P = (K + 1) / 2;
   const Tables<R> tb = tables<R>(sp);
   const Launch l = launch_cfg<R>(n);
-  const int64_t J = std::min<int64_t>(kPairChunk, P);
-  sp.work_a.reserve(size_t(batch) * plane * sizeof(C));
-  sp.work_b.reserve(size_t(batch) * size_t(J) * plane * sizeof(C));
-  C* S = sp.work_a.as<C>();  // accumulated spectrum, bit-reversed order
+  // pairs in chunks of kPairChunk (a fixed, batch-independent reduction
+  // order); a wave of chunks is transformed and accumulated concurrently,
+  // each chunk into its own partial spectrum
+  const int64_t nch = (P + kPairChunk - 1) / kPairChunk;
+  const int64_t chunk_bytes = batch * int64_t(kPairChunk) * plane * int64_t(sizeof(C));
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(nch, (int64_t(1) << 30) / chunk_bytes));
+  sp.work_a.reserve(size_t(batch * nch) * plane * sizeof(C));
+  sp.work_b.reserve(size_t(std::max<int64_t>(batch * std::min(cap * kPairChunk, P), batch)) * plane * sizeof(C));
+  C* Sp = sp.work_a.as<C>();  // per-chunk partial spectra, bit-reversed order
   C* Wk = sp.work_b.as<C>();
-  RK_CUDA(cudaMemsetAsync(S, 0, size_t(batch) * plane * sizeof(C), st));
   smem_opt_in(col_acc_kernel<R>, l.col_smem);
-  for (int64_t j0 = 0; j0 < P; j0 += J) {  // ascending pairs: a fixed reduction order
-    const int64_t nj = std::min(J, P - j0);
-    row_fwd<T, R>(coeff, sub, RowSrc{1, nj, j0, K}, batch * nj, logn, l, tb.tw, Wk, st);
+  for (int64_t c0 = 0; c0 < nch; c0 += cap) {
+    const int64_t ncw = std::min(cap, nch - c0), p0 = c0 * kPairChunk, np = std::min(ncw * kPairChunk, P - p0);
+    row_fwd<T, R>(coeff, sub, RowSrc{1, np, p0, K}, batch * np, logn, l, tb.tw, Wk, st);
     KernelTimer t(RK_KERNEL_SHEARLET, st);
-    col_acc_kernel<R><<<unsigned(batch * l.per_plane_cols), l.threads, l.col_smem, st>>>(Wk, nj, j0, logn, tb.tw,
-                                                                                         tb.mult2, S);
+    col_acc_kernel<R><<<unsigned(batch * l.per_plane_cols * ncw), l.threads, l.col_smem, st>>>(
+        Wk, np, p0, P, c0, ncw, nch, logn, tb.tw, tb.mult2, Sp);
     RK_CUDA(cudaGetLastError());
   }
-  // image = Re(ifft2(S)) / (n n)
-  col<R>(S, 2, batch, logn, l, tb, 0, 1, Wk, st);
+  // image = Re(ifft2(sum of the partials)) / (n n)
+  col<R>(Sp, 3, batch, logn, l, tb, 0, nch, Wk, st);
   row_inv<T, R>(Wk, RowDst{0, 0, 1, 1}, batch, logn, l, tb.tw, R(1) / R(plane), image, AdmmStore{}, st);
 }
 
