@@ -75,6 +75,7 @@ __device__ __forceinline__ C cmul_conj(C a, C b) {  // a * conj(b)
 
 constexpr int kTileMin = 4096;  // complex elements per CTA tile (>= one row, <= one plane)
 constexpr int kPerThread = 16;  // tile elements per thread
+constexpr int kAccPerThread = 8;  // synthesis accumulation: tile elements per thread (2x the threads, half the registers)
 constexpr int kPairChunk = 8;   // coefficient pairs per synthesis accumulation (fixed: batch-independent order)
 
 // shared-memory slot of tile element e (row e >> logn of the tile, swizzled within the row)
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src,
     }
   }
   const int64_t base = lr0 * n;
+#pragma unroll 4
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     R re = ld_r<R>(in0 + base + e), im = R(0);
     if (s0) re = re - ld_r<R>(s0 + base + e);  // sub(z1, u1) (admm.cpp:147)
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* _
   const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
   const int64_t base = lr0 * n;
   const C* src = in + p * plane + base;
+#pragma unroll 4
   for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[srow(e, logn)] = src[e];
   __syncthreads();
   ifft_dit_seq(sm, nr, n, logn, tw);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __res
 // throughout, so the sum order per bin is fixed and batch-independent.
 // W holds the wave's pairs p0 .. p0 + np - 1 of every image (b * np + pair - p0).
 template <class R>
-__global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* __restrict__ W, int64_t np, int64_t p0,
+__global__ void __launch_bounds__(512, 2) col_acc_kernel(const typename Cx<R>::T* __restrict__ W, int64_t np, int64_t p0,
                                                        int64_t P, int64_t c0, int64_t ncw, int64_t nch, int logn,
                                                        const typename Cx<R>::T* __restrict__ tw,
                                                        const typename Cx<R>::T* __restrict__ mult2,
@@ -302,21 +305,24 @@ __global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* _
   const int64_t plane = int64_t(n) * n;
   const int tile = tile_of(n), tc = tile / n;
   const int tiles = n / tc;
-  const int64_t cw = blockIdx.x % ncw, bt = blockIdx.x / ncw;
-  const int64_t b = bt / tiles;
-  const int c0t = int(bt - b * tiles) * tc;
+  // image fastest: the CTAs of one (chunk, tile) run together and share the
+  // chunk's multiplier tiles in L2
+  const int64_t batch = gridDim.x / (int64_t(tiles) * ncw);
+  const int64_t b = blockIdx.x % batch, ct = blockIdx.x / batch;
+  const int64_t cw = ct / tiles;
+  const int c0t = int(ct - cw * tiles) * tc;
   const int64_t chunk = c0 + cw;
   const int64_t ja = chunk * kPairChunk, jb = min(ja + kPairChunk, P);
-  C acc[kPerThread];
+  C acc[kAccPerThread];
 #pragma unroll
-  for (int m = 0; m < kPerThread; ++m) acc[m] = {R(0), R(0)};
+  for (int m = 0; m < kAccPerThread; ++m) acc[m] = {R(0), R(0)};
   for (int64_t j = ja; j < jb; ++j) {
     load_cols(sm, W + (b * np + (j - p0)) * plane, n, tc, c0t, ld);
     __syncthreads();
     fft_dif_seq(sm, tc, ld, logn, tw);
     const C* mk = mult2 + j * plane;
 #pragma unroll
-    for (int m = 0; m < kPerThread; ++m) {
+    for (int m = 0; m < kAccPerThread; ++m) {
       const int e = threadIdx.x + m * blockDim.x;
       if (e >= tile) break;
       const int r = e / tc, c = e - r * tc;
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(512) col_acc_kernel(const typename Cx<R>::T* _
   }
   C* s = Sp + (b * nch + chunk) * plane;
 #pragma unroll
-  for (int m = 0; m < kPerThread; ++m) {
+  for (int m = 0; m < kAccPerThread; ++m) {
     const int e = threadIdx.x + m * blockDim.x;
     if (e >= tile) break;
     const int r = e / tc, c = e - r * tc;
@@ -501,7 +507,8 @@ void backward_impl(Shearlet& sp, const T* coeff, const T* sub, int64_t batch, T*
     const int64_t ncw = std::min(cap, nch - c0), p0 = c0 * kPairChunk, np = std::min(ncw * kPairChunk, P - p0);
     row_fwd<T, R>(coeff, sub, RowSrc{1, np, p0, K}, batch * np, logn, l, tb.tw, Wk, st);
     KernelTimer t(RK_KERNEL_SHEARLET, st);
-    col_acc_kernel<R><<<unsigned(batch * l.per_plane_cols * ncw), l.threads, l.col_smem, st>>>(
+    col_acc_kernel<R><<<unsigned(batch * l.per_plane_cols * ncw), unsigned(std::max(32, l.tile / kAccPerThread)),
+                        l.col_smem, st>>>(
         Wk, np, p0, P, c0, ncw, nch, logn, tb.tw, tb.mult2, Sp);
     RK_CUDA(cudaGetLastError());
   }
