@@ -73,6 +73,7 @@ void check_device_filter(const rk_filter* f) {
 // Device-pointer bodies, reused by the host-buffer pipelines with their own scratch.
 void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
                   rk::DeviceBuffer& pkt, cudaStream_t st) {
+  rk::ensure_forward_schedule(p);
   pk.reserve(packed_image_bytes(p, batch));
   rk::launch_pack_images(dtype, d_image, batch, p.s, pk.as<float4>(), st);
   if (p.fwd.any_transposed) {

@@ -44,12 +44,14 @@ struct Pt {
 
 inline Pt to_pixel(double x, double y, double half) { return {x + half + 0.5, half - y + 0.5}; }
 
-// Bank-conflict cost of one layout: sum over quarter warps and taps of the
+// Bank-conflict costs of the layouts of one orientation: for every tap order
+// (swap: 0 none, 1 odd lanes load the bottom row first, 2 odd lanes load the
+// right column first — the kernel issues each lane's four taps in that order)
+// and row-pitch residue mod 8, the sum over quarter warps and taps of the
 // number of distinct 16-byte cells that share a slot (1 = conflict free).
-// swap: 0 none, 1 odd lanes load the bottom row first, 2 odd lanes load the
-// right column first (the kernel issues each lane's four taps in that order).
-double conflict_cost(const std::vector<Pt>& lanes_at_step, bool transposed, int pitch, int swap) {
-  double cost = 0.0;
+void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, double cost[3][8]) {
+  for (int sw = 0; sw < 3; ++sw)
+    for (int r = 0; r < 8; ++r) cost[sw][r] = 0.0;
   const int nw = int(lanes_at_step.size()) / 32;
   for (int w = 0; w < nw; ++w) {
     for (int q = 0; q < 32; q += 8) {
@@ -65,24 +67,29 @@ double conflict_cost(const std::vector<Pt>& lanes_at_step, bool transposed, int 
         lane_of[used] = q + l;
         ++used;
       }
-      for (int tap = 0; tap < 4; ++tap) {
-        int64_t addr[8];
-        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int worst = used ? 1 : 0;
-        for (int u = 0; u < used; ++u) {
-          const bool odd = (lane_of[u] & 1) != 0;
-          const int dy = (swap == 1 && odd) ? 1 - (tap >> 1) : (tap >> 1);
-          const int dx = (swap == 2 && odd) ? 1 - (tap & 1) : (tap & 1);
-          addr[u] = (bi[u] + dy) * pitch + bj[u] + dx;
-          bool dup = false;
-          for (int v = 0; v < u && !dup; ++v) dup = addr[v] == addr[u];
-          if (!dup) worst = std::max(worst, ++cnt[int(((addr[u] % 8) + 8) % 8)]);
+      if (!used) continue;
+      for (int sw = 0; sw < 3; ++sw)
+        for (int tap = 0; tap < 4; ++tap) {
+          int64_t ti[8], tj[8];
+          bool first[8];
+          for (int u = 0; u < used; ++u) {
+            const bool odd = (lane_of[u] & 1) != 0;
+            ti[u] = bi[u] + ((sw == 1 && odd) ? 1 - (tap >> 1) : (tap >> 1));
+            tj[u] = bj[u] + ((sw == 2 && odd) ? 1 - (tap & 1) : (tap & 1));
+            first[u] = true;
+            for (int v = 0; v < u && first[u]; ++v) first[u] = !(ti[v] == ti[u] && tj[v] == tj[u]);
+          }
+          for (int r = 0; r < 8; ++r) {
+            const int64_t pitch = 64 + r;
+            int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int worst = 1;
+            for (int u = 0; u < used; ++u)
+              if (first[u]) worst = std::max(worst, ++cnt[int((((ti[u] * pitch + tj[u]) % 8) + 8) % 8)]);
+            cost[sw][r] += worst;
+          }
         }
-        cost += worst;
-      }
     }
   }
-  return cost;
 }
 
 // Conflict-free reference for conflict_cost: one wavefront per quarter warp
@@ -286,14 +293,16 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
             sim.push_back(q);
           }
       }
-      for (int tr = 0; tr < 2; ++tr)
+      if (mapping == 0) cp.ideal = ideal_cost(sim);
+      for (int tr = 0; tr < 2; ++tr) {
+        double costs[3][8];
+        conflict_costs(sim, tr == 1, costs);
         for (int swap = 0; swap < 3; ++swap)
           for (int res = 0; res < 8; ++res) {
-            const double c = conflict_cost(sim, tr == 1, 64 + res, swap) *
-                             (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
+            const double c = costs[swap][res] * (1.0 + 1e-3 * tr + 1e-5 * swap + 1e-4 * mapping);
             if (c < best) best = c, cp.tr = tr, cp.residue = res, cp.swap = swap, cp.mapping = mapping;
-            if (mapping == 0 && tr == 0 && swap == 0 && res == 0) cp.ideal = ideal_cost(sim);
           }
+      }
     }
     cp.cost = best;
     cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);

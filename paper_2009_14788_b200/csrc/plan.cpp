@@ -10,6 +10,7 @@
 #include <complex>
 #include <cstring>
 #include <limits>
+#include <mutex>
 
 #include "rk_internal.hpp"
 
@@ -111,28 +112,11 @@ RayD setup_ray(int64_t s, double ox, double oy, double dx, double dy, double tmi
   return r;
 }
 
-}  // namespace
-
-// Tile geometry of the backprojection kernel (kernels.cu): 32 x 32 pixels.
-constexpr int kBpTile = 32;
-
-void build_plan(Plan& p) {
+// forward_parallel_t / forward_fanbeam_t ray setup (projector.cpp:95-139), fp64.
+std::vector<RayD> compute_rays(const Plan& p, const std::vector<double2>& trig, int64_t* total_samples) {
   const rk_geometry& g = p.g;
-  p.s = g.image_size;
-  p.na = g.n_angles;
-  p.nd = g.det_count;
-  if (!(g.step > 0.0)) throw ValidationError("projector step must be positive");  // projector.cpp:31-33
-  if (p.s > 32768) throw ValidationError("image_size " + std::to_string(p.s) + " exceeds the supported 32768");
-  if (p.na * p.nd > (int64_t(1) << 31)) throw ValidationError("n_angles * det_count exceeds 2^31 rays");
-
   const int64_t s = p.s, na = p.na, nd = p.nd;
   const bool fan = g.kind == RK_FANBEAM;
-
-  // angle_trig (projector.cpp:89-93)
-  std::vector<double2> trig(static_cast<size_t>(na));
-  for (int64_t a = 0; a < na; ++a) trig[size_t(a)] = make_double2(std::cos(p.angles[size_t(a)]), std::sin(p.angles[size_t(a)]));
-
-  // ----- forward ray table: forward_parallel_t / forward_fanbeam_t ray setup
   std::vector<RayD> rays(static_cast<size_t>(na * nd));
   const double inf = std::numeric_limits<double>::infinity();
   int64_t total = 0;
@@ -159,10 +143,73 @@ void build_plan(Plan& p) {
       total += r.n;
     }
   }
+  if (total_samples) *total_samples = total;
+  return rays;
+}
+
+std::vector<double2> angle_trig(const Plan& p) {  // projector.cpp:89-93
+  std::vector<double2> trig(static_cast<size_t>(p.na));
+  for (int64_t a = 0; a < p.na; ++a)
+    trig[size_t(a)] = make_double2(std::cos(p.angles[size_t(a)]), std::sin(p.angles[size_t(a)]));
+  return trig;
+}
+
+}  // namespace
+
+// The forward schedule (fwd_plan.cpp) and per-ray records, built and uploaded
+// once, on the first forward projection through the plan.
+void ensure_forward_schedule(Plan& p) {
+  if (p.device < 0) return;  // host-only plans schedule eagerly and never launch
+  std::call_once(p.fwd_once, [&] {
+    std::vector<RayD> rays = compute_rays(p, angle_trig(p), nullptr);
+    std::vector<float4> rg, ra;
+    build_forward_plan(p, rays, rg, ra);
+    RK_CUDA(cudaSetDevice(p.device));
+    p.ray_geom.reserve(rg.size() * sizeof(float4));
+    p.ray_aux.reserve(ra.size() * sizeof(float4));
+    RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(p.ray_aux.ptr, ra.data(), ra.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    p.fwd_boxes.reserve(p.fwd.boxes.size() * sizeof(int4));
+    p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int4));
+    RK_CUDA(cudaMemcpy(p.fwd_boxes.ptr, p.fwd.boxes.data(), p.fwd.boxes.size() * sizeof(int4),
+                       cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    p.fwd_warps.reserve(p.fwd.warps.size() * sizeof(int2));
+    RK_CUDA(cudaMemcpy(p.fwd_warps.ptr, p.fwd.warps.data(), p.fwd.warps.size() * sizeof(int2),
+                       cudaMemcpyHostToDevice));
+  });
+}
+
+// Tile geometry of the backprojection kernel (kernels.cu): 32 x 32 pixels.
+constexpr int kBpTile = 32;
+
+void build_plan(Plan& p) {
+  const rk_geometry& g = p.g;
+  p.s = g.image_size;
+  p.na = g.n_angles;
+  p.nd = g.det_count;
+  if (!(g.step > 0.0)) throw ValidationError("projector step must be positive");  // projector.cpp:31-33
+  if (p.s > 32768) throw ValidationError("image_size " + std::to_string(p.s) + " exceeds the supported 32768");
+  if (p.na * p.nd > (int64_t(1) << 31)) throw ValidationError("n_angles * det_count exceeds 2^31 rays");
+
+  const int64_t s = p.s, na = p.na, nd = p.nd;
+  const bool fan = g.kind == RK_FANBEAM;
+
+  const std::vector<double2> trig = angle_trig(p);
+
+  // ----- forward ray table (exact per-image work); the forward schedule is
+  // built on the first forward call (ensure_forward_schedule): FBP-only and
+  // backprojection-only users never pay for its planning
+  int64_t total = 0;
+  std::vector<RayD> rays = compute_rays(p, trig, &total);
   p.forward_samples = total;
-  // per-ray records for the kernel + the chunk / box schedule (fwd_plan.cpp)
-  std::vector<float4> rg, ra;
-  build_forward_plan(p, rays, rg, ra);
+  if (p.device < 0) {  // host-only plan (inspection): schedule now
+    std::vector<float4> rg, ra;
+    build_forward_plan(p, rays, rg, ra);
+  }
+  rays.clear();
+  rays.shrink_to_fit();
+  const double inf = std::numeric_limits<double>::infinity();
 
   // ----- backprojection staging window: the widest detector footprint of a
   // 32x32 pixel tile over all tiles and angles (+ one cell on each side for
@@ -235,17 +282,7 @@ void build_plan(Plan& p) {
   // ----- upload (device < 0: host-only plan, used for inspection on machines without a GPU)
   if (p.device < 0) return;
   RK_CUDA(cudaSetDevice(p.device));
-  p.ray_geom.reserve(rg.size() * sizeof(float4));
-  p.ray_aux.reserve(ra.size() * sizeof(float4));
   p.trig.reserve(trig.size() * sizeof(double2));
-  RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(p.ray_aux.ptr, ra.data(), ra.size() * sizeof(float4), cudaMemcpyHostToDevice));
-  p.fwd_boxes.reserve(p.fwd.boxes.size() * sizeof(int4));
-  p.fwd_cta.reserve(p.fwd.cta.size() * sizeof(int4));
-  RK_CUDA(cudaMemcpy(p.fwd_boxes.ptr, p.fwd.boxes.data(), p.fwd.boxes.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(p.fwd_cta.ptr, p.fwd.cta.data(), p.fwd.cta.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  p.fwd_warps.reserve(p.fwd.warps.size() * sizeof(int2));
-  RK_CUDA(cudaMemcpy(p.fwd_warps.ptr, p.fwd.warps.data(), p.fwd.warps.size() * sizeof(int2), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
   p.bp_tile_window.reserve(tile_window.size() * sizeof(int));
   RK_CUDA(cudaMemcpy(p.bp_tile_window.ptr, tile_window.data(), tile_window.size() * sizeof(int),

@@ -90,6 +90,10 @@ struct Plan;
 void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<float4>& ray_geom,
                         std::vector<float4>& ray_aux);
 
+// Builds and uploads the plan's forward schedule once (plan.cpp); every
+// forward launch path calls it first.
+void ensure_forward_schedule(Plan& p);
+
 struct Plan {
   int device = 0;
   rk_geometry g{};              // resolved; g.angles -> angles.data()
@@ -103,7 +107,8 @@ struct Plan {
   // forward schedule (fwd_plan.cpp): CTA = A angles x W detectors; the rays
   // are marched chunk by chunk along t, each chunk's image footprint (box) is
   // staged in shared memory
-  ForwardSchedule fwd;
+  ForwardSchedule fwd;      // built on the first forward call (ensure_forward_schedule)
+  std::once_flag fwd_once;
   DeviceBuffer fwd_boxes;  // int4 per chunk (see ForwardSchedule::boxes)
   DeviceBuffer fwd_cta;    // int4 per CTA
   DeviceBuffer fwd_warps;  // int2 {angle, first detector} per (cta, warp); angle -1 = idle
