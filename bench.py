@@ -110,7 +110,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_images_per_s(wl, budget_s=12.0, warmup=1, fixed_batch=None):
+def cpu_reference_images_per_s(wl, budget_s=15.0, warmup=1, fixed_batch=None):
     """The reference (oracle/_ref: radonkit compiled in place) forward + backprojection
     on this host's cores, all threads, on a bounded sample of the workload."""
     from oracle import Geom, RefOracle, default_oracle
@@ -138,11 +138,11 @@ def cpu_reference_images_per_s(wl, budget_s=12.0, warmup=1, fixed_batch=None):
     t1 = run(1)  # also the warm-up
     for _ in range(max(0, warmup - 1)):
         run(1)
-    b = fixed_batch or max(1, min(64, int(budget_s / 3.0 / max(t1, 1e-3))))
-    times = [run(b) for _ in range(3)]
+    b = fixed_batch or max(1, min(64, int(budget_s / 5.0 / max(t1, 1e-3))))
+    times = [run(b) for _ in range(5)]  # 1 warm-up + >= 5 timed runs, median
     med = statistics.median(times)
     return {"value": b / med, "unit": "images/s", "cores": cores, "kind": kind,
-            "sample": f"{b} x {s}^2 image(s), {na} angles, {nd} cells per run; median of 3 runs after 1 warm-up; "
+            "sample": f"{b} x {s}^2 image(s), {na} angles, {nd} cells per run; median of 5 runs after 1 warm-up; "
                       f"{'parallel' if k == 'parallel' else 'fan-beam'}; set_num_threads({cores})"}
 
 
