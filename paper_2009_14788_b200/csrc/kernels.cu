@@ -401,6 +401,22 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kTile + tx;
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile;
+  // Tile-relative (row, column) of the thread's r-th pixel.  Parallel beam: a
+  // warp is one row of 32 pixels (adjacent pixels read adjacent detector
+  // cells, conflict free).  Fan beam: magnification up to span / (sp (D_so -
+  // R)) spreads a row of 8 pixels over more than 8 cells, so a quarter warp
+  // takes a 4 x 2 block (a warp an 8 x 4 block; block w * RPT + r of the
+  // tile's 32), which keeps its cells within one bank period.
+  auto pixel_of = [&](int t, int r, int& pr, int& pc) {
+    if constexpr (KIND == kBpParallel) {
+      pr = (t >> 5) + r * (kTile / RPT);
+      pc = t & 31;
+    } else {
+      const int l = t & 31, qq = l >> 3, e = l & 7, blk = (t >> 5) * RPT + r;
+      pc = 8 * (blk & 3) + 4 * (qq & 1) + (e & 3);
+      pr = 4 * (blk >> 2) + 2 * (qq >> 1) + (e >> 2);
+    }
+  };
   const int64_t g = blockIdx.z;
   const double half = 0.5 * double(s);
   const double off = 0.5 * double(nd) - 0.5;
@@ -483,28 +499,23 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
     __syncthreads();
     // ---- accumulate
     const double kmag = span / spacing;
-    const float lx = float(tx);
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
       const Cell* w = win + q * window;
-      // the pixel's column terms, shared by the thread's pixels (same value in
-      // the packed and single-lane kernels: only lx enters)
-      float col0 = 0.f, col1 = 0.f;
-      if constexpr (KIND == kBpParallel) {
-        col0 = fmaf(lx, k.cx, k.base);
-      } else if constexpr (KIND == kBpFan32) {
-        col0 = k.a * lx;
-        col1 = fmaf(k.c, lx, k.den00);
-      }
+      // parallel: the column term is shared by the thread's pixels (one column)
+      float col0 = 0.f;
+      if constexpr (KIND == kBpParallel) col0 = fmaf(float(tx), k.cx, k.base);
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const float ly = float(ty + r * (kTile / RPT));
+        int pr, pc;
+        pixel_of(tid, r, pr, pc);
+        const float lx = float(pc), ly = float(pr);
         float kf;
         if constexpr (KIND == kBpParallel) {
           kf = fmaf(ly, k.cy, col0);
         } else if constexpr (KIND == kBpFan32) {
-          const float num = fmaf(k.b, ly, col0);  // (qx - qx00) K - u00 (den - den00)
-          const float den = fmaf(k.d, ly, col1);  // qy + D_so
+          const float num = fmaf(k.b, ly, k.a * lx);             // (qx - qx00) K - u00 (den - den00)
+          const float den = fmaf(k.d, ly, fmaf(k.c, lx, k.den00));  // qy + D_so
           kf = fmaf(num, rcp_approx(den), k.base);
         } else {
           const double dlx = double(lx), dly = double(ly);
@@ -536,7 +547,9 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
   const int P = s + 2;
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int i = i0 + ty + r * (kTile / RPT), j = j0 + tx;
+    int pr, pc;
+    pixel_of(tid, r, pr, pc);
+    const int i = i0 + pr, j = j0 + pc;
     if (i >= s || j >= s) continue;
     if (epi.mode == kOutUser) {
       const float v[kPack] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
