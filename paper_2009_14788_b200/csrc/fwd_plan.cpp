@@ -154,6 +154,8 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   const double t_lo = (fan ? p.g.source_distance : 0.0) - R - 1.0;
   const double t_hi = (fan ? p.g.source_distance : 0.0) + R + 1.0;
   const int64_t nkb = (nd + 31) / 32;  // 32-cell detector blocks
+  const char* pce = std::getenv("RK_FWD_CHUNK_LAYOUT");
+  const bool per_chunk_layout = !(pce && pce[0] == '0');
   int64_t budget = F.box_budget;
 
   struct Shape {
@@ -192,8 +194,12 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
 
   // Greedy chunking of one CTA for a layout: returns false if even the
   // shortest chunk overflows the budget.  Appends {r0|c0<<16, rows|cols<<16, pitch, t_end bits}.
-  auto chunk_cta = [&](const int2* wa, bool tr, int residue, std::vector<int4>* out, int64_t* staged,
-                       int64_t* max_cells) -> bool {
+  // refine (optional): per-chunk layout {tr, residue, swap} for the chunk
+  // [t, tb] with box b; the CTA-wide layout when it returns false or its box
+  // would not fit.
+  using Refine = std::function<bool(double, double, int*, int*, int*)>;
+  auto chunk_cta = [&](const int2* wa, bool tr, int residue, int swap, std::vector<int4>* out, int64_t* staged,
+                       int64_t* max_cells, bool* any_tr, const Refine& refine) -> bool {
     double t = t_lo;
     while (t < t_hi) {
       bool placed = false;
@@ -206,17 +212,28 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           placed = true;
           break;
         }
-        const int64_t rows = tr ? b.cols : b.rows, cols = tr ? b.rows : b.cols;
-        const int pitch = pitch_for(cols, residue);
+        int64_t rows = tr ? b.cols : b.rows, cols = tr ? b.rows : b.cols;
+        int pitch = pitch_for(cols, residue);
         if (rows * pitch > budget && len > 2.0) continue;
         if (rows * pitch > budget) return false;
+        bool ctr = tr;
+        int cswap = swap;
+        int ctr_i = tr, cres = residue, csw = swap;
+        if (refine && refine(t, tb, &ctr_i, &cres, &csw)) {
+          const int64_t rr = ctr_i ? b.cols : b.rows, cc = ctr_i ? b.rows : b.cols;
+          const int pp = pitch_for(cc, cres);
+          if (rr * pp <= budget) ctr = ctr_i != 0, cswap = csw, rows = rr, cols = cc, pitch = pp;
+        }
         if (out) {
-          const int64_t r0 = tr ? b.c0 : b.r0, c0 = tr ? b.r0 : b.c0;
+          const int64_t r0 = ctr ? b.c0 : b.r0, c0 = ctr ? b.r0 : b.c0;
           float tend = tb >= t_hi ? INFINITY : float(tb);
           int tbits;
           std::memcpy(&tbits, &tend, 4);
-          out->push_back(make_int4(int(r0 | (c0 << 16)), int(rows | (cols << 16)), pitch, tbits));
+          // pitch | orientation << 16 | tap order << 17 (kernels.cu)
+          out->push_back(make_int4(int(r0 | (c0 << 16)), int(rows | (cols << 16)),
+                                   pitch | (int(ctr) << 16) | (cswap << 17), tbits));
         }
+        if (any_tr) *any_tr |= ctr;
         if (staged) *staged += rows * cols;
         if (max_cells) *max_cells = std::max(*max_cells, rows * pitch);
         t = tb;
@@ -248,6 +265,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     bool ok = false;
     int64_t staged = 0, max_cells = 0;
     double cost = 0.0, ideal = 0.0;  // simulated wavefronts: chosen layout, conflict-free
+    bool any_tr = false;             // some chunk stages the transposed image
     std::vector<int4> boxes;
   };
   // Layout (lane mapping, orientation, pitch, tap order) by simulation, then
@@ -305,7 +323,51 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       }
     }
     cp.cost = best;
-    cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, &cp.boxes, &cp.staged, &cp.max_cells);
+    // Per-chunk layout: the lane lines' bank pattern drifts along the march
+    // (sample stagger; fan beam: ray spacing grows with the distance to the
+    // source), so each chunk re-picks orientation, pitch and tap order for
+    // the CTA's lane mapping from a few steps inside it.
+    std::vector<Pt> csim;
+    const int mp = cp.mapping;
+    Refine refine = [&](double ta, double tb, int* tr_o, int* res_o, int* sw_o) {
+      csim.clear();
+      for (int st = 0; st < 3; ++st) {
+        const double tt = ta + (tb - ta) * (0.2 + 0.3 * st);
+        for (int w = 0; w < 8; ++w)
+          for (int l = 0; l < 32; ++l) {
+            Pt q{NAN, NAN};
+            int a;
+            int64_t kk;
+            lane_ray(mp, w, l, a, kk);
+            if (a >= 0 && kk < nd) {
+              const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
+              if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
+                const double m = std::floor((tt - ry.t0) / ry.h);
+                const double t = ry.t0 + (m + 0.5) * ry.h;
+                q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
+              }
+            }
+            csim.push_back(q);
+          }
+      }
+      double bc = 1e300;
+      for (int tr = 0; tr < 2; ++tr) {
+        double costs[3][8];
+        conflict_costs(csim, tr == 1, costs);
+        for (int sw = 0; sw < 3; ++sw)
+          for (int res = 0; res < 8; ++res) {
+            // ties keep the CTA-wide layout (no needless switches)
+            const bool same = tr == cp.tr && res == cp.residue && sw == cp.swap;
+            const double c = costs[sw][res] * (same ? 1.0 : 1.0 + 1e-3);
+            if (c < bc) bc = c, *tr_o = tr, *res_o = res, *sw_o = sw;
+          }
+      }
+      return bc < 1e300;
+    };
+    bool any_tr = false;
+    cp.ok = chunk_cta(wa, cp.tr == 1, cp.residue, cp.swap, &cp.boxes, &cp.staged, &cp.max_cells, &any_tr,
+                      per_chunk_layout ? refine : Refine());
+    cp.any_tr = any_tr;
   };
   auto plan_shape = [&](Shape sh, std::vector<CtaPlan>& plans) {
     std::vector<int2> warps = warps_of(sh);
@@ -404,7 +466,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       F.boxes.insert(F.boxes.end(), cp.boxes.begin(), cp.boxes.end());
       F.max_box = std::max(F.max_box, cp.max_cells);
       F.staged_texels += cp.staged;
-      F.any_transposed |= cp.tr == 1;
+      F.any_transposed |= cp.any_tr;
     }
     if (std::getenv("RK_DEBUG_PLAN")) {
       int64_t ntr = 0;

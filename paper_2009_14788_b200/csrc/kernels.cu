@@ -199,26 +199,22 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   const int a = __ldg(warps + cta * (kFwdThreads / 32) + slot).x;
   const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
-  const bool tr = (cfg.z & 1) != 0;
-  // Per-lane tap order chosen by the planner against bank conflicts: odd lanes
-  // issue the bottom row first (swap 1) or the right column first (swap 2).
-  // Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA) (rowB,colB); the
-  // weights follow the same order, so no value is moved between registers.
-  const int swap = (cfg.z >> 1) & 3;
+  // Per-chunk layout chosen by the planner against bank conflicts (box record
+  // z = pitch | orientation << 16 | tap order << 17): chunks of transposed
+  // orientation stage the transposed packed image with x and y swapped, and
+  // odd lanes issue the bottom row first (tap order 1) or the right column
+  // first (2).  Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA) (rowB,colB);
+  // the weights follow the same order, so no value is moved between registers.
   const bool odd = (threadIdx.x & 1) != 0;
-  const bool rs = swap == 1 && odd, cs = swap == 2 && odd;
-  const int dX = cs ? -1 : 1;
   float4 G = make_float4(0.f, 0.f, 0.f, 0.f), X = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     G = __ldg(ray_geom + r);
     X = __ldg(ray_aux + r);
   }
-  const float px0 = tr ? G.y : G.x, py0 = tr ? G.x : G.y;
-  const float hx = tr ? G.w : G.z, hy = tr ? G.z : G.w;
   const int n = __float_as_int(X.y);
   const float t0 = X.z, inv_h = X.w;
   const int P = s + 2;
-  const float4* src = (tr ? img_t : img) + g * int64_t(P) * P;
+  const int64_t goff = g * int64_t(P) * P;
   const int4* bxs = boxes + cfg.x;
 
   if (threadIdx.x == 0) {
@@ -234,9 +230,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   const int box_cells = lane_box;  // LANE: the second box's offset (max box cells of the plan)
   auto stage_lane = [&](int cc_, float* dst) {
     const int4 b = __ldg(bxs + cc_);
-    const int br0 = b.x & 0xffff, bc0 = b.x >> 16, brows = b.y & 0xffff, bcols = b.y >> 16, bpitch = b.z;
+    const int br0 = b.x & 0xffff, bc0 = b.x >> 16, brows = b.y & 0xffff, bcols = b.y >> 16, bpitch = b.z & 0xffff;
+    const float4* bsrc = (((b.z >> 16) & 1) ? img_t : img) + goff;
     for (int rr = warp; rr < brows; rr += kFwdThreads / 32) {
-      const float4* row = src + int64_t(br0 + rr) * P + bc0;
+      const float4* row = bsrc + int64_t(br0 + rr) * P + bc0;
       for (int cc = lane; cc < bcols; cc += 32) cp_async4(dst + rr * bpitch + cc, row + cc);
     }
     cp_async_commit();
@@ -246,7 +243,14 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   }
   for (int c = 0; c < cfg.y; ++c) {
     const int4 bx = __ldg(bxs + c);  // CTA-uniform
-    const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16, pitch = bx.z;
+    const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16, pitch = bx.z & 0xffff;
+    const bool tr = ((bx.z >> 16) & 1) != 0;
+    const int swap = (bx.z >> 17) & 3;
+    const bool rs = swap == 1 && odd, cs = swap == 2 && odd;
+    const int dX = cs ? -1 : 1;
+    const float px0 = tr ? G.y : G.x, py0 = tr ? G.x : G.y;
+    const float hx = tr ? G.w : G.z, hy = tr ? G.z : G.w;
+    const float4* src = (tr ? img_t : img) + goff;
     const float tend = __int_as_float(bx.w);
     // samples of this chunk: t_m < t_end  <=>  m < ceil((t_end - t0) / h - 0.5)
     const int m_end =
