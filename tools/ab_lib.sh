@@ -8,5 +8,5 @@ for L in "$1" "$2"; do
   RK_LIB=$L timeout 300 python bench.py --workload $WL --no-cpu-baseline --no-extras --no-e2e 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); pk=d['roofline']['per_kernel']
 print(round(d['value']), 'fwd', round(pk['forward']['ms'],3), 'bp', round(pk['backproject']['ms'],3))"
-  RK_LIB=$L timeout 300 ncu --metrics $M --clock-control none -k regex:forward_kernel -c 1 --csv python tools/prof_step.py $WL 1 32 2>/dev/null | grep -E '"(gpu__|l1tex|smsp|sm__)' | awk -F'","' '{print $(NF-2), $NF}'
+  RK_LIB=$L timeout 300 ncu --metrics $M --clock-control none -k regex:${KREGEX:-forward_kernel} -c 1 --csv python tools/prof_step.py $WL 1 32 2>/dev/null | grep -E '"(gpu__|l1tex|smsp|sm__)' | awk -F'","' '{print $(NF-2), $NF}'
 done
