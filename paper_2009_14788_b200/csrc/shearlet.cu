@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src,
     }
   }
   const int64_t base = lr0 * n;
-#pragma unroll 4
+#pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     R re = ld_r<R>(in0 + base + e), im = R(0);
     if (s0) re = re - ld_r<R>(s0 + base + e);  // sub(z1, u1) (admm.cpp:147)
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src,
   __syncthreads();
   fft_dif_seq(sm, nr, n, logn, tw);
   C* o = out + p * plane + base;
+#pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) o[e] = sm[srow(e, logn)];
 }
 
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* _
   const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
   const int64_t base = lr0 * n;
   const C* src = in + p * plane + base;
-#pragma unroll 4
+#pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[srow(e, logn)] = src[e];
   __syncthreads();
   ifft_dit_seq(sm, nr, n, logn, tw);
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* _
     o0 = (b * m.K + k0) * plane;
     if (k0 + 1 < m.K) o1 = o0 + plane;
   }
+#pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     const C v = sm[srow(e, logn)];
     const R re = v.x * scale, im = v.y * scale;
@@ -223,6 +225,7 @@ __host__ __device__ inline int col_ld(int n) { return n + 4; }
 
 template <class C>
 __device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int n, int tc, int c0, int ld) {
+#pragma unroll 8
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
     sm[c * ld + fft_swz(r)] = src[int64_t(r) * n + c0 + c];
@@ -230,6 +233,7 @@ __device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int 
 }
 template <class C>
 __device__ __forceinline__ void store_cols(C* __restrict__ dst, const C* sm, int n, int tc, int c0, int ld) {
+#pragma unroll 8
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
     dst[int64_t(r) * n + c0 + c] = sm[c * ld + fft_swz(r)];
@@ -258,12 +262,14 @@ __global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __res
     const int64_t q = q0 + p, j = q / B, b = q % B;
     const C* src = in + b * plane;
     const C* mk = mult2 + j * plane;
+  #pragma unroll 8
     for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
       const int r = e / tc, c = e - r * tc;
       const int64_t gi = int64_t(r) * n + c0 + c;
       sm[c * ld + fft_swz(r)] = cmul(src[gi], mk[gi]);
     }
   } else if (mode == 3) {
+  #pragma unroll 8
     for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
       const int r = e / tc, c = e - r * tc;
       const int64_t gi = int64_t(r) * n + c0 + c;
