@@ -75,10 +75,15 @@ void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, vo
                   rk::DeviceBuffer& pkt, cudaStream_t st) {
   rk::ensure_forward_schedule(p);
   pk.reserve(packed_image_bytes(p, batch));
-  rk::launch_pack_images(dtype, d_image, batch, p.s, pk.as<float4>(), st);
+  const bool h8 = rk::use_h8(dtype, batch);
+  if (h8)
+    rk::launch_pack_images_h8(d_image, batch, p.s, pk.as<float4>(), st);
+  else
+    rk::launch_pack_images(dtype, d_image, batch, p.s, pk.as<float4>(), st);
   if (p.fwd.any_transposed) {
     pkt.reserve(packed_image_bytes(p, batch));
-    rk::launch_transpose_images(pk.as<float4>(), batch, p.s, pkt.as<float4>(), st);
+    rk::launch_transpose_images(pk.as<float4>(), h8 ? rk::groups_of_h8(batch) : rk::groups_of(batch), p.s,
+                                pkt.as<float4>(), st);
   }
   rk::launch_forward(p, pk.as<float4>(), pkt.as<float4>(), batch, dtype, d_sino, st);
 }
@@ -86,7 +91,10 @@ void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, vo
 void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
                       rk::DeviceBuffer& pk, cudaStream_t st) {
   pk.reserve(packed_sino_bytes(p, batch));
-  rk::launch_pack_sino(dtype, d_sino, batch, p.na, p.nd, pk.as<float4>(), st);
+  if (rk::use_h8(dtype, batch))
+    rk::launch_pack_sino_h8(d_sino, batch, p.na, p.nd, pk.as<float4>(), st);
+  else
+    rk::launch_pack_sino(dtype, d_sino, batch, p.na, p.nd, pk.as<float4>(), st);
   rk::launch_backproject(p, pk.as<float4>(), batch, dtype, d_image, st);
 }
 

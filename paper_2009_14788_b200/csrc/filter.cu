@@ -12,6 +12,8 @@
 // conjugate twiddles (bit-reversed in, natural out): no permutation pass.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "fft_smem.cuh"
 #include "rk_internal.hpp"
 
@@ -39,7 +41,10 @@ __device__ __forceinline__ double st_cast<double>(float v) { return double(v); }
 
 constexpr int kFilterThreads = 256;
 
-template <class TIn, class TOut, bool PACKED>
+// PACKED 0: user layout; 1: packed float4 cells (four images); 2: half of a
+// packed half8 cell (fp16 storage, use_h8): this CTA's four rows are images
+// 4g .. 4g+3, i.e. the low or high 8 bytes of group g / 2's cells.
+template <class TIn, class TOut, int PACKED>
 __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
                                                                 int nd, int P, int logP,
                                                                 const float* __restrict__ resp,
@@ -88,7 +93,14 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
   for (int k = threadIdx.x; k < nd; k += blockDim.x) {
     const float2 x = za[fft_swz(k)], y = zb[fft_swz(k)];
     const float v[4] = {(x.x * inv) * scale, (x.y * inv) * scale, (y.x * inv) * scale, (y.y * inv) * scale};
-    if (PACKED) {
+    if (PACKED == 2) {
+      // four halves: exactly the values the float4 path narrows through fp16
+      const __half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]), h2 = __float2half_rn(v[2]),
+                   h3 = __float2half_rn(v[3]);
+      const uint2 bits = make_uint2(unsigned(__half_as_ushort(h0)) | (unsigned(__half_as_ushort(h1)) << 16),
+                                    unsigned(__half_as_ushort(h2)) | (unsigned(__half_as_ushort(h3)) << 16));
+      reinterpret_cast<uint2*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + k) * 2 + (g & 1)] = bits;
+    } else if (PACKED == 1) {
       // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows
       // to the storage precision first (sino_filter.cpp:123, 126-128)
       packed[(g * na + a) * int64_t(nd) + k] =
@@ -124,7 +136,9 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
   dispatch(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = packed_out ? filter_kernel<T, T, true> : filter_kernel<T, T, false>;
+    auto kern = packed_out ? filter_kernel<T, T, 1> : filter_kernel<T, T, 0>;
+    if constexpr (std::is_same<T, __half>::value)
+      if (packed_out && use_h8(dtype, batch)) kern = filter_kernel<T, T, 2>;
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FILTER, st);
     kern<<<grid, kFilterThreads, smem, st>>>(static_cast<const T*>(in), batch, int(n_angles), int(f.det_count), P,

@@ -86,6 +86,58 @@ __global__ void pack_sino_kernel(const T* __restrict__ src, int64_t batch, int64
   }
 }
 
+// ---- fp16 storage: eight images per 16-byte texel (kPackH8)
+__device__ __forceinline__ unsigned h2_bits(__half lo, __half hi) {
+  return unsigned(__half_as_ushort(lo)) | (unsigned(__half_as_ushort(hi)) << 16);
+}
+// word w of a half8 texel -> images 2w, 2w+1 as floats (exact)
+__device__ __forceinline__ float2 h8_pair(unsigned w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+__device__ __forceinline__ unsigned h8_word(const uint4& u, int i) {
+  return i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w;
+}
+
+// image [B][s][s] half -> [G8][s+2][s+2] half8 texels with a zero border
+__global__ void pack_images_h8_kernel(const __half* __restrict__ src, int64_t batch, int s, uint4* __restrict__ dst) {
+  const int P = s + 2;
+  const int64_t plane = int64_t(P) * P;
+  const int64_t g = blockIdx.y;
+  const __half z = __float2half_rn(0.f);
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < plane;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int pi = int(idx / P), pj = int(idx % P);
+    __half v[kPackH8];
+#pragma unroll
+    for (int q = 0; q < kPackH8; ++q) v[q] = z;
+    if (pi >= 1 && pi <= s && pj >= 1 && pj <= s) {
+      const int64_t off = int64_t(pi - 1) * s + (pj - 1);
+#pragma unroll
+      for (int q = 0; q < kPackH8; ++q) {
+        const int64_t b = g * kPackH8 + q;
+        if (b < batch) v[q] = src[b * int64_t(s) * s + off];
+      }
+    }
+    dst[g * plane + idx] = make_uint4(h2_bits(v[0], v[1]), h2_bits(v[2], v[3]), h2_bits(v[4], v[5]), h2_bits(v[6], v[7]));
+  }
+}
+
+// sino [B][na*nd] half -> [G8][na*nd] half8 texels
+__global__ void pack_sino_h8_kernel(const __half* __restrict__ src, int64_t batch, int64_t plane, uint4* __restrict__ dst) {
+  const int64_t g = blockIdx.y;
+  const __half z = __float2half_rn(0.f);
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < plane;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    __half v[kPackH8];
+#pragma unroll
+    for (int q = 0; q < kPackH8; ++q) {
+      const int64_t b = g * kPackH8 + q;
+      v[q] = b < batch ? src[b * plane + idx] : z;
+    }
+    dst[g * plane + idx] = make_uint4(h2_bits(v[0], v[1]), h2_bits(v[2], v[3]), h2_bits(v[4], v[5]), h2_bits(v[6], v[7]));
+  }
+}
+
 // ------------------------------------------------------------------ forward
 // packed image -> transposed packed image, 32x32-texel tiles through shared
 // memory (coalesced both ways).
@@ -168,7 +220,9 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // every tap is a 32-bit shared load: a quarter of the shared-memory traffic
 // and FMAs of the packed loop, with the same operations on lane 0 in the same
 // order, so its results equal the packed kernel's bit for bit.
-template <class TOut, bool LANE>
+// H8 (fp16 storage, batch > 1): half8 texels, eight images per lane, each tap
+// load converted to fp32 pairs; per image the same operations and order.
+template <class TOut, bool LANE, bool H8 = false>
 __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
@@ -223,6 +277,9 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   }
   __syncthreads();
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float a8[H8 ? kPackH8 : 1];
+#pragma unroll
+  for (int q = 0; q < (H8 ? kPackH8 : 1); ++q) a8[q] = 0.f;
   int m = 0;
   // LANE: lane 0 of the box's texels by 4-byte cp.async (warp w takes rows w,
   // w + 8, ...) into two alternating scalar boxes, the next chunk's copies in
@@ -296,6 +353,16 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
         const float v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
         a0 = fmaf(w1, v1, fmaf(w2, v2, fmaf(w3, v3, fmaf(w4, v4, a0))));
         continue;
+      } else if constexpr (H8) {
+        const uint4* q8 = reinterpret_cast<const uint4*>(box_s) + (i * pitch + j + dA);
+        const uint4 u1 = q8[0], u2 = q8[dX], u3 = q8[dY], u4 = q8[dY + dX];
+#pragma unroll
+        for (int wd = 0; wd < 4; ++wd) {
+          const float2 f1 = h8_pair(h8_word(u1, wd)), f2 = h8_pair(h8_word(u2, wd));
+          const float2 f3 = h8_pair(h8_word(u3, wd)), f4 = h8_pair(h8_word(u4, wd));
+          a8[2 * wd] = fmaf(w1, f1.x, fmaf(w2, f2.x, fmaf(w3, f3.x, fmaf(w4, f4.x, a8[2 * wd]))));
+          a8[2 * wd + 1] = fmaf(w1, f1.y, fmaf(w2, f2.y, fmaf(w3, f3.y, fmaf(w4, f4.y, a8[2 * wd + 1]))));
+        }
       } else {
       const float4* q = box_s + (i * pitch + j + dA);
       const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
@@ -308,6 +375,15 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   }
   if (!valid) return;
   const float h = X.x;
+  if constexpr (H8) {  // user layout only (fp16 storage)
+    const int64_t n_rays8 = int64_t(na) * nd;
+#pragma unroll
+    for (int q = 0; q < kPackH8; ++q) {
+      const int64_t b = g * kPackH8 + q;
+      if (b < batch) sino[b * n_rays8 + r] = from_f32<TOut>(a8[q] * h);
+    }
+    return;
+  }
   const float acc[kPack] = {a0 * h, a1 * h, a2 * h, a3 * h};
   const int64_t n_rays = int64_t(na) * nd;
   if (epi.mode == kOutUser) {
@@ -384,15 +460,18 @@ constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 // threads x 2 pixels, so the 32x32 tiles of one image fill the GPU.  Per
 // pixel the operations on lane 0 and their order are the packed kernel's
 // (same tile-relative constants), so the results are bit-identical.
-template <int KIND, class TOut, bool LANE>
-__global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == kBpParallel ? 4 : 3))
+// H8 (fp16 storage, batch > 1): half8 cells, eight images per pixel, 512
+// threads x 2 pixels (the accumulators of eight images), each tap load
+// converted to fp32 pairs; per image the same operations and order.
+template <int KIND, class TOut, bool LANE, bool H8 = false>
+__global__ void __launch_bounds__((LANE || H8) ? 512 : kBpThreads, (LANE || H8) ? 2 : (KIND == kBpParallel ? 4 : 3))
     backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
     int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
   using Cell = typename std::conditional<LANE, float, float4>::type;
-  constexpr int RPT = LANE ? 2 : kRowsPerThread;  // pixels (rows) per thread
+  constexpr int RPT = (LANE || H8) ? 2 : kRowsPerThread;  // pixels (rows) per thread
   constexpr int NT = kTile * kTile / RPT;         // threads
   extern __shared__ float4 smem_raw[];
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
@@ -433,6 +512,11 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
   float4 acc[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc8[H8 ? RPT : 1][H8 ? kPackH8 : 1];
+#pragma unroll
+  for (int r = 0; r < (H8 ? RPT : 1); ++r)
+#pragma unroll
+    for (int q = 0; q < (H8 ? kPackH8 : 1); ++q) acc8[r][q] = 0.f;
 
   for (int a0 = 0; a0 < na; a0 += chunk) {
     const int nac = min(chunk, na - a0);
@@ -536,6 +620,15 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
         if constexpr (LANE) {
           const float s0 = w[c0], s1 = w[c0 + 1];
           acc[r].x = fmaf(wt, s1, fmaf(wl, s0, acc[r].x));
+        } else if constexpr (H8) {
+          const float4 s0f = w[c0], s1f = w[c0 + 1];
+          const uint4 s0 = *reinterpret_cast<const uint4*>(&s0f), s1 = *reinterpret_cast<const uint4*>(&s1f);
+#pragma unroll
+          for (int wd = 0; wd < 4; ++wd) {
+            const float2 f0 = h8_pair(h8_word(s0, wd)), f1 = h8_pair(h8_word(s1, wd));
+            acc8[r][2 * wd] = fmaf(wt, f1.x, fmaf(wl, f0.x, acc8[r][2 * wd]));
+            acc8[r][2 * wd + 1] = fmaf(wt, f1.y, fmaf(wl, f0.y, acc8[r][2 * wd + 1]));
+          }
         } else {
           const float4 s0 = w[c0], s1 = w[c0 + 1];
           acc[r].x = fmaf(wt, s1.x, fmaf(wl, s0.x, acc[r].x));
@@ -555,6 +648,14 @@ __global__ void __launch_bounds__(LANE ? 512 : kBpThreads, LANE ? 2 : (KIND == k
     pixel_of(tid, r, pr, pc);
     const int i = i0 + pr, j = j0 + pc;
     if (i >= s || j >= s) continue;
+    if constexpr (H8) {  // user layout only (fp16 storage)
+#pragma unroll
+      for (int q = 0; q < kPackH8; ++q) {
+        const int64_t b = g * kPackH8 + q;
+        if (b < batch) out[(b * s + i) * int64_t(s) + j] = from_f32<TOut>(acc8[r][q]);
+      }
+      continue;
+    }
     if (epi.mode == kOutUser) {
       const float v[kPack] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
 #pragma unroll
@@ -617,9 +718,36 @@ void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int
   RK_CUDA(cudaGetLastError());
 }
 
-void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st) {
+void launch_pack_images_h8(const void* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st) {
+  const int64_t plane = (s + 2) * (s + 2);
+  dim3 grid(std::min<unsigned>(blocks_for(plane, 256), 4096u), unsigned(groups_of_h8(batch)));
+  KernelTimer timer(RK_KERNEL_PACK, st);
+  pack_images_h8_kernel<<<grid, 256, 0, st>>>(static_cast<const __half*>(src), batch, int(s),
+                                              reinterpret_cast<uint4*>(dst));
+  RK_CUDA(cudaGetLastError());
+}
+
+void launch_pack_sino_h8(const void* src, int64_t batch, int64_t na, int64_t nd, float4* dst, cudaStream_t st) {
+  const int64_t plane = na * nd;
+  dim3 grid(std::min<unsigned>(blocks_for(plane, 256), 4096u), unsigned(groups_of_h8(batch)));
+  KernelTimer timer(RK_KERNEL_PACK, st);
+  pack_sino_h8_kernel<<<grid, 256, 0, st>>>(static_cast<const __half*>(src), batch, plane,
+                                            reinterpret_cast<uint4*>(dst));
+  RK_CUDA(cudaGetLastError());
+}
+
+// RK_H8=0 keeps fp16 storage on the float4 layout (A/B).
+bool use_h8(int dtype, int64_t batch) {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_H8");
+    return !(e && e[0] == '0');
+  }();
+  return on && dtype == RK_F16 && batch > 1;
+}
+
+void launch_transpose_images(const float4* src, int64_t groups, int64_t s, float4* dst, cudaStream_t st) {
   const int P = int(s + 2);
-  dim3 grid(unsigned((P + 31) / 32), unsigned((P + 31) / 32), unsigned(groups_of(batch)));
+  dim3 grid(unsigned((P + 31) / 32), unsigned((P + 31) / 32), unsigned(groups));
   KernelTimer timer(RK_KERNEL_PACK, st);
   transpose_images_kernel<<<grid, dim3(32, 8), 0, st>>>(src, P, dst);
   RK_CUDA(cudaGetLastError());
@@ -637,11 +765,14 @@ static bool single_lane(int64_t batch) {
 void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
   const ForwardSchedule& F = p.fwd;
-  dim3 grid(unsigned(F.cta.size()), unsigned(groups_of(batch)));
+  const bool h8 = epi.mode == kOutUser && use_h8(dtype, batch);
+  dim3 grid(unsigned(F.cta.size()), unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     const bool lane = single_lane(batch);
     auto kern = lane ? forward_kernel<T, true> : forward_kernel<T, false>;
+    if constexpr (std::is_same<T, __half>::value)
+      if (h8) kern = forward_kernel<T, false, true>;
     const size_t smem = size_t(F.max_box) * (lane ? 2 * sizeof(float) : sizeof(float4));
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_FORWARD, st);
@@ -656,9 +787,10 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
 void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch, int dtype, void* image,
                         cudaStream_t st, BpEpilogue epi) {
   const int tiles = int((p.s + kTile - 1) / kTile);
-  dim3 grid(tiles, tiles, unsigned(groups_of(batch)));
+  const bool h8 = epi.mode == kOutUser && use_h8(dtype, batch);
+  dim3 grid(tiles, tiles, unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
   const bool lane = single_lane(batch);
-  dim3 block(kTile, kTile / (lane ? 2 : kRowsPerThread));
+  dim3 block(kTile, kTile / ((lane || h8) ? 2 : kRowsPerThread));
   const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
   const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
   const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
@@ -670,6 +802,11 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                      : (kind == kBpParallel ? backproject_kernel<kBpParallel, T, false>
                         : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false>
                                             : backproject_kernel<kBpFan64, T, false>);
+    if constexpr (std::is_same<T, __half>::value)
+      if (h8)
+        kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, true>
+               : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, true>
+                                   : backproject_kernel<kBpFan64, T, false, true>;
     if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,

@@ -62,6 +62,14 @@ constexpr int kPack = 4;
 
 inline int64_t groups_of(int64_t batch) { return (batch + kPack - 1) / kPack; }
 
+// fp16 storage (user-facing projector / FBP calls, batch > 1): eight images
+// per 16-byte texel, stored as half — exact, because the values are halves
+// already — so each shared-memory tap load serves twice the images; the
+// arithmetic stays fp32 and per image identical to the float4 layout.
+constexpr int kPackH8 = 8;
+inline int64_t groups_of_h8(int64_t batch) { return (batch + kPackH8 - 1) / kPackH8; }
+bool use_h8(int dtype, int64_t batch);
+
 // ----------------------------------------------------------------- forward schedule
 // fp64 ray after the reference's clip prologue (projector.cpp:66-78)
 struct RayD {
@@ -226,6 +234,8 @@ int filter_kind_from_name(const std::string& name);
 // ----------------------------------------------------------------- launchers (kernels.cu / filter.cu)
 // All launchers enqueue on `stream` and never synchronise.
 void launch_pack_images(int dtype, const void* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
+void launch_pack_images_h8(const void* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
+void launch_pack_sino_h8(const void* src, int64_t batch, int64_t na, int64_t nd, float4* dst, cudaStream_t st);
 void launch_pack_sino(int dtype, const void* src, int64_t batch, int64_t na, int64_t nd, float4* dst,
                       cudaStream_t st);
 // Kernel epilogues.  kOutUser: user layout in the storage dtype (the default
@@ -250,7 +260,7 @@ struct BpEpilogue {
 };
 
 // packed image -> its transpose ([G][s+2][s+2], rows <-> columns)
-void launch_transpose_images(const float4* src, int64_t batch, int64_t s, float4* dst, cudaStream_t st);
+void launch_transpose_images(const float4* src, int64_t groups, int64_t s, float4* dst, cudaStream_t st);
 // packed_image_t is only read when the schedule has transposed CTAs
 void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi = FwdEpilogue{});

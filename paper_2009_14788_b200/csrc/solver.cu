@@ -241,7 +241,7 @@ void dot(const float4* a, const float4* b, int64_t groups, int64_t plane, double
 // forward of a packed image (+ its transpose when the schedule needs one)
 void apply_forward(Plan& p, const float4* x, float4* xt, int64_t batch, FwdEpilogue epi, cudaStream_t st) {
   ensure_forward_schedule(p);
-  if (p.fwd.any_transposed) launch_transpose_images(x, batch, p.s, xt, st);
+  if (p.fwd.any_transposed) launch_transpose_images(x, groups_of(batch), p.s, xt, st);
   launch_forward(p, x, xt, batch, RK_F32, nullptr, st, epi);
 }
 
