@@ -3,6 +3,7 @@
 // (cited), enqueues the CUDA work and maps exceptions onto rk_status codes.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -111,7 +112,9 @@ void check_dtype(int dtype) { (void)rk::dtype_size(dtype); }
 // ------------------------------------------------------------------ host pipelines
 // Reference-shaped calls (host Tensor in, host Tensor out): the batch is cut
 // into chunks of whole packed groups, and chunk i+1's host->device copy, chunk
-// i's kernels and chunk i-1's device->host copy overlap on two streams.
+// i's kernels and chunk i-1's device->host copy overlap on three streams (each
+// stream runs copy-in, kernels, copy-out of its chunk in order, so two streams
+// would cap the throughput at one chunk per half of that sum).
 bool is_pinned(const void* p) {
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
@@ -137,7 +140,7 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
   min_items = (min_items + rk::kPack - 1) / rk::kPack * rk::kPack;
   chunk = std::min(batch, std::max(chunk, min_items));
   const bool pinned_in = is_pinned(h_in), pinned_out = is_pinned(h_out);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < rk::Plan::kPipeSlots; ++i) {
     p.pipe_in[i].reserve(size_t(chunk) * in_item);
     p.pipe_out[i].reserve(size_t(chunk) * out_item);
   }
@@ -166,7 +169,7 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
     RK_CUDA(cudaMemcpyAsync(dst, p.pipe_out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
     if (!pinned_in || !pinned_out) RK_CUDA(cudaStreamSynchronize(st));
     b0 += nb;
-    slot ^= 1;
+    slot = (slot + 1) % rk::Plan::kPipeSlots;
   }
   for (auto s : p.copy_streams) RK_CUDA(cudaStreamSynchronize(s));
 }

@@ -133,8 +133,9 @@ struct Plan {
   DeviceBuffer packed_image, packed_image_t, packed_sino;
   cudaEvent_t scratch_free = nullptr;
   // host-buffer (*_host) pipelines: two streams, each with its own buffers
-  cudaStream_t copy_streams[2] = {nullptr, nullptr};
-  DeviceBuffer pipe_in[2], pipe_out[2], pipe_pk[2], pipe_pkt[2];
+  static constexpr int kPipeSlots = 3;  // chunks in flight: copy-in, kernels, copy-out overlap
+  cudaStream_t copy_streams[kPipeSlots] = {nullptr, nullptr, nullptr};
+  DeviceBuffer pipe_in[kPipeSlots], pipe_out[kPipeSlots], pipe_pk[kPipeSlots], pipe_pkt[kPipeSlots];
   // solver scratch
   DeviceBuffer solver_a, solver_b, solver_c, solver_d, solver_scalars;
 
