@@ -358,7 +358,7 @@ def main():
         bi = 4 * nb * (s * s + na * nd)
         e2e = {"value": B * args.steps / el, "unit": "images/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi,
                "ms_per_step": 1e3 * el / args.steps,
-               "path": "rk_forward_host + rk_backproject_host (pinned host buffers, 2-stream chunked copy/compute "
+               "path": "rk_forward_host + rk_backproject_host (pinned host buffers, 3-stream chunked copy/compute "
                        "pipeline, synchronous like the reference's Tensor-in/Tensor-out calls)"}
 
     cpu = None
