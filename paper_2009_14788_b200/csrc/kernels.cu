@@ -336,10 +336,13 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const int jmax = cols - 2, imax = rows - 2;
     const int dA = (rs ? pitch : 0) + (cs ? 1 : 0);
     const int dY = rs ? -pitch : pitch;
+    // chunk-relative entry point: the box origin is an integer, so the shift
+    // is exact and the per-sample position one FMA
+    const float pxc = px0 - ox, pyc = py0 - oy;
     for (; m < m_end; ++m) {
       const float t = float(m) + 0.5f;
-      const float px = fmaf(t, hx, px0) - ox;  // exact shift: the box origin is an integer
-      const float py = fmaf(t, hy, py0) - oy;
+      const float px = fmaf(t, hx, pxc);
+      const float py = fmaf(t, hy, pyc);
       const float fj = floorf(px), fi = floorf(py);
       const float fx = px - fj, fy = py - fi;
       const int j = min(max(int(fj), 0), jmax);
