@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <stdexcept>
 #include <thread>
 
 #include "rk_internal.hpp"
@@ -110,6 +111,65 @@ struct Box {
 };
 
 inline int pitch_for(int64_t cols, int residue) { return int(cols + ((residue - cols) % 8 + 8) % 8); }
+
+// Replays the forward kernel's per-lane schedule on the host in the kernel's
+// own fp32 arithmetic (std::fma == FFMA; kernels.cu, forward_kernel) and
+// checks that every sample's four taps lie inside its chunk's staged box and
+// that the chunks partition each ray's samples — the invariant that lets the
+// kernel index the box without clamping.  RK_VERIFY_PLAN=1 (tests).
+void verify_forward_schedule(const Plan& p, const std::vector<float4>& ray_geom, const std::vector<float4>& ray_aux) {
+  const ForwardSchedule& F = p.fwd;
+  const int64_t nd = p.nd;
+  for (size_t cta = 0; cta < F.cta.size(); ++cta) {
+    const int4 cfg = F.cta[cta];
+    const int lq = (cfg.z >> 3) & 3;
+    const int2* wa = &F.warps[cta * 8];
+    for (int t = 0; t < 256; ++t) {
+      int slot = t >> 5, k;
+      if (lq == 0) {
+        k = wa[t >> 5].y + (t & 31);
+      } else {
+        const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
+        const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
+        slot = (ag << lq) + aq;
+        k = wa[0].y + cg * (8 >> lq) + cq;
+      }
+      const int a = wa[slot].x;
+      if (a < 0 || k >= nd) continue;
+      const size_t r = size_t(int64_t(a) * nd + k);
+      const float4 G = ray_geom[r], X = ray_aux[r];
+      int n;
+      std::memcpy(&n, &X.y, 4);
+      const float t0 = X.z, inv_h = X.w;
+      int m = 0;
+      for (int c = 0; c < cfg.y; ++c) {
+        const int4 bx = F.boxes[size_t(cfg.x + c)];
+        const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16;
+        const bool tr = ((bx.z >> 16) & 1) != 0;
+        float tend;
+        std::memcpy(&tend, &bx.w, 4);
+        const int m_end =
+            std::isinf(tend) ? n : std::min(std::max(int(std::ceil(std::fma(tend - t0, inv_h, -0.5f))), 0), n);
+        const float pxc = (tr ? G.y : G.x) - float(c0), pyc = (tr ? G.x : G.y) - float(r0);
+        const float hx = tr ? G.w : G.z, hy = tr ? G.z : G.w;
+        for (; m < m_end; ++m) {
+          const float tt = float(m) + 0.5f;
+          const float px = std::fma(tt, hx, pxc), py = std::fma(tt, hy, pyc);
+          const int j = int(std::floor(px)), i = int(std::floor(py));
+          if (j < 0 || i < 0 || j + 1 >= cols || i + 1 >= rows) {
+            char msg[256];
+            std::snprintf(msg, sizeof(msg),
+                          "forward schedule: ray (angle %d, cell %d) sample %d leaves box %d of CTA %zu "
+                          "(tap %d,%d of %dx%d)",
+                          a, k, m, c, cta, i, j, rows, cols);
+            throw std::logic_error(msg);
+          }
+        }
+      }
+      if (m != n) throw std::logic_error("forward schedule: chunks do not cover every sample of a ray");
+    }
+  }
+}
 
 }  // namespace
 
@@ -468,6 +528,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       F.staged_texels += cp.staged;
       F.any_transposed |= cp.any_tr;
     }
+    if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
     if (std::getenv("RK_DEBUG_PLAN")) {
       int64_t ntr = 0;
       for (const int4& c : F.cta) ntr += c.z & 1;

@@ -1,0 +1,43 @@
+"""Forward-schedule invariant (CPU, host-only plans): replaying the forward
+kernel's per-lane schedule in its own fp32 arithmetic, every sample's four
+taps lie inside its chunk's staged box and the chunks cover every sample of
+every ray (fwd_plan.cpp: verify_forward_schedule).  The kernel indexes the
+box without clamping on the strength of this invariant."""
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import math, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2009_14788_b200 as rk
+rng = np.random.default_rng(7)
+cases = [
+    rk.make_parallel(256, rk.angles_linspace(0.0, math.pi, 256)),                      # config 1
+    rk.make_parallel(512, rk.angles_linspace(0.0, math.pi, 512)),                      # config 2
+    rk.make_fanbeam(512, rk.angles_linspace(0.0, 2 * math.pi, 512), 512.0),            # config 3
+    rk.make_parallel(100, rk.angles_linspace(0.0, math.pi, 33), 77, 1.3),
+    rk.make_parallel(64, list(rng.uniform(-10, 10, 50)), 96, 0.7),                     # scattered angles
+    rk.make_parallel(96, [(i * 100.0 / 64 - 50.0) * math.pi / 180 for i in range(64)]),  # limited arc
+    rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * math.pi, 64), 70.0, det_distance=300.0),  # source close
+    rk.make_fanbeam(80, list(rng.uniform(0, 7, 40)), 60.0, det_distance=150.0, det_count=101),
+]
+for g in cases:
+    rk.get_plan(g, None, -1)
+rk.get_plan(rk.make_parallel(48, rk.angles_linspace(0.0, math.pi, 30)), rk.ProjectorOptions(0.37), -1)
+print("schedules verified", len(cases) + 1)
+"""
+
+
+def test_forward_schedule_boxes_contain_every_sample():
+    env = dict(os.environ, RK_VERIFY_PLAN="1")
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0 and "schedules verified" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
