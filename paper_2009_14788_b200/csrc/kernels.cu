@@ -211,15 +211,18 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // tap of four images each), weights shared by the four images.  Samples are
 // visited in ascending m, so each output is a fixed-order fp32 sum.
 // Chunk membership: m < ceil((T_{c+1} - t0) / h - 0.5), evaluated in fp32;
-// the boxes carry one unit of slack in t, so rounding never leaves a sample
-// outside its box.  CTAs whose lanes spread mostly along image columns read
-// the transposed packed image with x and y swapped (bilinear is symmetric).
+// the boxes carry one unit of slack in t and a texel around the taps, so no
+// sample leaves its box (proved per plan by RK_VERIFY_PLAN, fwd_plan.cpp) and
+// the tap indices need no clamping.  Chunks whose lane lines run mostly along
+// image columns stage the transposed packed image with x and y swapped
+// (bilinear is symmetric).
 //
 // LANE (batch 1): only lane 0 of the packed group carries an image, so the box
-// is staged as scalars (lane 0 of each texel, cooperative 16-byte loads) and
-// every tap is a 32-bit shared load: a quarter of the shared-memory traffic
-// and FMAs of the packed loop, with the same operations on lane 0 in the same
-// order, so its results equal the packed kernel's bit for bit.
+// is staged as scalars (lane 0 of each texel, 4-byte cp.async into two
+// alternating boxes) and every tap is a 32-bit shared load: a quarter of the
+// shared-memory traffic and FMAs of the packed loop, with the same operations
+// on lane 0 in the same order, so its results equal the packed kernel's bit
+// for bit.
 // H8 (fp16 storage, batch > 1): half8 texels, eight images per lane, each tap
 // load converted to fp32 pairs; per image the same operations and order.
 template <class TOut, bool LANE, bool H8 = false>
