@@ -220,6 +220,19 @@ def test_host_path_matches_device_path(rk, oracle, cuda):
     assert torch.equal(bh, rk.backprojection(g, dev(sh, cuda)).cpu())
 
 
+@pytest.mark.parametrize("dtype", [np.float16, np.float64])
+def test_host_path_matches_device_path_other_storage(rk, oracle, cuda, dtype):
+    """fp16 (half8 texels, chunked host pipeline with partial groups) and fp64
+    storage: host-buffer entry points == device entry points, bit for bit."""
+    for g in (par(rk, 48, 36), fan(rk, 48, 30, 96.0)):
+        img = batched_phantom(oracle, 48, 37).astype(dtype)
+        sd = host(rk.forward(g, dev(img, cuda)))
+        sh = rk.forward(g, img)
+        assert sh.dtype == dtype and np.array_equal(sd, sh)
+        assert np.array_equal(host(rk.backprojection(g, dev(sh, cuda))), rk.backprojection(g, sh))
+        assert np.array_equal(host(rk.fbp(g, dev(sh, cuda))), rk.fbp(g, sh))
+
+
 def test_half_accuracy_vs_single(rk, oracle, cuda):
     """acceptance.cpp:212-235 (C4) / test_projector.cpp:226-231: fp16 storage within 5e-4 of fp32."""
     g = par(rk, 256, 256)
