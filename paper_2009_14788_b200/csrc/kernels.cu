@@ -468,7 +468,7 @@ constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 // threads x 2 pixels (the accumulators of eight images), each tap load
 // converted to fp32 pairs; per image the same operations and order.
 template <int KIND, class TOut, bool LANE, bool H8 = false>
-__global__ void __launch_bounds__((LANE || H8) ? 512 : kBpThreads, (LANE || H8) ? 2 : (KIND == kBpParallel ? 4 : 3))
+__global__ void __launch_bounds__((LANE || H8) ? 512 : kBpThreads, (LANE || H8) ? 2 : (KIND == kBpFan64 ? 3 : 4))
     backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
