@@ -123,7 +123,7 @@ struct RowSrc {
   int64_t J, j0, K;
 };
 template <class T, class R>
-__global__ void __launch_bounds__(512) row_fwd_kernel(const T* __restrict__ src, const T* __restrict__ sub, RowSrc m,
+__global__ void __launch_bounds__(512, 3) row_fwd_kernel(const T* __restrict__ src, const T* __restrict__ sub, RowSrc m,
                                                        int logn, const typename Cx<R>::T* __restrict__ tw,
                                                        typename Cx<R>::T* __restrict__ out) {
   using C = typename Cx<R>::T;
@@ -177,7 +177,7 @@ struct RowDst {
   int64_t q0, B, K;
 };
 template <class T, class R>
-__global__ void __launch_bounds__(512) row_inv_kernel(const typename Cx<R>::T* __restrict__ in, RowDst m, int logn,
+__global__ void __launch_bounds__(512, 3) row_inv_kernel(const typename Cx<R>::T* __restrict__ in, RowDst m, int logn,
                                                        const typename Cx<R>::T* __restrict__ tw, R scale,
                                                        T* __restrict__ dst, AdmmStore admm) {
   using C = typename Cx<R>::T;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void store_cols(C* __restrict__ dst, const C* sm, int
 // mode 2: out = colDIT^-1(in)                       (plane p -> p)
 // mode 3: out = colDIT^-1(sum_c in[p][c])             (B = chunk partials per plane, summed in order)
 template <class R>
-__global__ void __launch_bounds__(512) col_kernel(const typename Cx<R>::T* __restrict__ in, int mode, int logn,
+__global__ void __launch_bounds__(512, 3) col_kernel(const typename Cx<R>::T* __restrict__ in, int mode, int logn,
                                                    const typename Cx<R>::T* __restrict__ tw,
                                                    const typename Cx<R>::T* __restrict__ mult2, int64_t q0, int64_t B,
                                                    typename Cx<R>::T* __restrict__ out) {
