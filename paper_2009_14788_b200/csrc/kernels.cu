@@ -198,6 +198,20 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Blackwell packed FP32 FMA (FFMA2): two independent fmaf's in one instruction,
+// each rounded exactly as fmaf — so pairs of images share one issue slot and
+// the results are bit-identical to the scalar chain.  The broadcast weight
+// becomes FFMA2's scalar operand.
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  float2 aa = make_float2(a, a);
+  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&aa), rb = *reinterpret_cast<unsigned long long*>(&b),
+                     rc = *reinterpret_cast<unsigned long long*>(&c), rd;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
+}
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+
 constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (lanes)
 
 // Ray-driven forward projection (projector.cpp:66-139), one CTA per block of
@@ -279,10 +293,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  float a8[H8 ? kPackH8 : 1];
+  float2 a01 = make_float2(0.f, 0.f), a23 = a01;  // images 0-1, 2-3 (LANE: a01.x)
+  float2 a8[H8 ? kPackH8 / 2 : 1];                 // H8: image pairs
 #pragma unroll
-  for (int q = 0; q < (H8 ? kPackH8 : 1); ++q) a8[q] = 0.f;
+  for (int q = 0; q < (H8 ? kPackH8 / 2 : 1); ++q) a8[q] = make_float2(0.f, 0.f);
   int m = 0;
   // LANE: lane 0 of the box's texels by 4-byte cp.async (warp w takes rows w,
   // w + 8, ...) into two alternating scalar boxes, the next chunk's copies in
@@ -355,7 +369,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
       if constexpr (LANE) {
         const float* q = box1 + (i * pitch + j + dA);
         const float v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
-        a0 = fmaf(w1, v1, fmaf(w2, v2, fmaf(w3, v3, fmaf(w4, v4, a0))));
+        a01.x = fmaf(w1, v1, fmaf(w2, v2, fmaf(w3, v3, fmaf(w4, v4, a01.x))));
         continue;
       } else if constexpr (H8) {
         const uint4* q8 = reinterpret_cast<const uint4*>(box_s) + (i * pitch + j + dA);
@@ -364,16 +378,15 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
         for (int wd = 0; wd < 4; ++wd) {
           const float2 f1 = h8_pair(h8_word(u1, wd)), f2 = h8_pair(h8_word(u2, wd));
           const float2 f3 = h8_pair(h8_word(u3, wd)), f4 = h8_pair(h8_word(u4, wd));
-          a8[2 * wd] = fmaf(w1, f1.x, fmaf(w2, f2.x, fmaf(w3, f3.x, fmaf(w4, f4.x, a8[2 * wd]))));
-          a8[2 * wd + 1] = fmaf(w1, f1.y, fmaf(w2, f2.y, fmaf(w3, f3.y, fmaf(w4, f4.y, a8[2 * wd + 1]))));
+          // scalar FMAs: the converted halves are not register pairs, FFMA2 measured slower here
+          a8[wd].x = fmaf(w1, f1.x, fmaf(w2, f2.x, fmaf(w3, f3.x, fmaf(w4, f4.x, a8[wd].x))));
+          a8[wd].y = fmaf(w1, f1.y, fmaf(w2, f2.y, fmaf(w3, f3.y, fmaf(w4, f4.y, a8[wd].y))));
         }
       } else {
       const float4* q = box_s + (i * pitch + j + dA);
       const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
-      a0 = fmaf(w1, v1.x, fmaf(w2, v2.x, fmaf(w3, v3.x, fmaf(w4, v4.x, a0))));
-      a1 = fmaf(w1, v1.y, fmaf(w2, v2.y, fmaf(w3, v3.y, fmaf(w4, v4.y, a1))));
-      a2 = fmaf(w1, v1.z, fmaf(w2, v2.z, fmaf(w3, v3.z, fmaf(w4, v4.z, a2))));
-      a3 = fmaf(w1, v1.w, fmaf(w2, v2.w, fmaf(w3, v3.w, fmaf(w4, v4.w, a3))));
+      a01 = ffma2(w1, lo2(v1), ffma2(w2, lo2(v2), ffma2(w3, lo2(v3), ffma2(w4, lo2(v4), a01))));
+      a23 = ffma2(w1, hi2(v1), ffma2(w2, hi2(v2), ffma2(w3, hi2(v3), ffma2(w4, hi2(v4), a23))));
       }
     }
   }
@@ -384,11 +397,11 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
 #pragma unroll
     for (int q = 0; q < kPackH8; ++q) {
       const int64_t b = g * kPackH8 + q;
-      if (b < batch) sino[b * n_rays8 + r] = from_f32<TOut>(a8[q] * h);
+      if (b < batch) sino[b * n_rays8 + r] = from_f32<TOut>((q & 1 ? a8[q >> 1].y : a8[q >> 1].x) * h);
     }
     return;
   }
-  const float acc[kPack] = {a0 * h, a1 * h, a2 * h, a3 * h};
+  const float acc[kPack] = {a01.x * h, a01.y * h, a23.x * h, a23.y * h};
   const int64_t n_rays = int64_t(na) * nd;
   if (epi.mode == kOutUser) {
 #pragma unroll
@@ -635,10 +648,9 @@ __global__ void __launch_bounds__((LANE || H8) ? 512 : kBpThreads, (LANE || H8) 
           }
         } else {
           const float4 s0 = w[c0], s1 = w[c0 + 1];
-          acc[r].x = fmaf(wt, s1.x, fmaf(wl, s0.x, acc[r].x));
-          acc[r].y = fmaf(wt, s1.y, fmaf(wl, s0.y, acc[r].y));
-          acc[r].z = fmaf(wt, s1.z, fmaf(wl, s0.z, acc[r].z));
-          acc[r].w = fmaf(wt, s1.w, fmaf(wl, s0.w, acc[r].w));
+          const float2 lo = ffma2(wt, lo2(s1), ffma2(wl, lo2(s0), lo2(acc[r])));
+          const float2 hi = ffma2(wt, hi2(s1), ffma2(wl, hi2(s0), hi2(acc[r])));
+          acc[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
       }
     }
