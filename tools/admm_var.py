@@ -1,3 +1,6 @@
+"""Run-to-run spread of the paper's ADMM on one image (512^2, 50 x 50): five back-to-back
+reconstructions in one process (the first ones run while the GPU clocks ramp).
+Usage: python tools/admm_var.py"""
 import math, sys, time, os
 sys.path.insert(0, os.getcwd())
 import torch, paper_2009_14788_b200 as rk

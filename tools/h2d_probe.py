@@ -1,3 +1,5 @@
+"""Pinned host -> device copy bandwidth (one copy, 2/4 concurrent streams, 8 MB chunks).
+Usage: python tools/h2d_probe.py"""
 import time, torch
 N = 128*512*512
 h = torch.rand(N).pin_memory()
