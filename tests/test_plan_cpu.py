@@ -29,6 +29,15 @@ cases = [
     rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * math.pi, 64), 70.0, det_distance=300.0),  # source close
     rk.make_fanbeam(80, list(rng.uniform(0, 7, 40)), 60.0, det_distance=150.0, det_count=101),
 ]
+for i in range(30):  # random geometries: sizes, angle lists, detectors, fan distances
+    s = int(rng.choice([3, 17, 40, 64, 97, 131, 200]))
+    ang = list(rng.uniform(-7.0, 7.0, int(rng.integers(1, 60))))
+    nd, sp = int(rng.integers(1, 3 * s + 8)), float(rng.uniform(0.3, 2.5))
+    if i % 2:
+        cases.append(rk.make_fanbeam(s, ang, float(s) * float(rng.uniform(0.75, 4.0)), float(rng.uniform(0.5, 3.0)) * s,
+                                     nd, sp))
+    else:
+        cases.append(rk.make_parallel(s, ang, nd, sp))
 for g in cases:
     rk.get_plan(g, None, -1)
 rk.get_plan(rk.make_parallel(48, rk.angles_linspace(0.0, math.pi, 30)), rk.ProjectorOptions(0.37), -1)

@@ -246,7 +246,7 @@ def test_half_accuracy_vs_single(rk, oracle, cuda):
 
 
 def _random_geometry(rk, rs, fan):
-    s = int(rs.choice([1, 2, 3, 5, 17, 40, 64, 97]))
+    s = int(rs.choice([1, 2, 3, 5, 17, 40, 64, 97, 131, 160]))
     na = int(rs.integers(1, 40))
     nd = int(rs.integers(1, 3 * s + 8))
     sp = float(rs.uniform(0.3, 2.5))
@@ -257,7 +257,7 @@ def _random_geometry(rk, rs, fan):
     return rk.make_fanbeam(s, ang, src, float(rs.uniform(0.5, 3.0)) * s, nd, sp)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(24))
 def test_random_geometry_parity(rk, oracle, cuda, seed):
     """Arbitrary angle lists, tiny and odd sizes, any detector count/spacing, fan distances, steps."""
     rs = np.random.default_rng(100 + seed)
