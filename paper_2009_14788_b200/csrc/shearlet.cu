@@ -29,7 +29,9 @@
 // non-finite flag), and synthesis can read (z1 - u1) instead of c.
 #include <cuda_fp16.h>
 
+#include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fft_smem.cuh"
 #include "rk_internal.hpp"
@@ -158,6 +160,33 @@ __global__ void __launch_bounds__(512, 3) row_fwd_kernel(const T* __restrict__ s
     }
   }
   const int64_t base = lr0 * n;
+  if constexpr (std::is_same<T, float>::value && std::is_same<R, float>::value) {
+    // four reals per 16-byte load (memory-level parallelism: the pass is
+    // latency-bound on its global reads); caller buffers may be misaligned
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(sub)) & 15) == 0;
+    if (n >= 4 && aligned) {
+#pragma unroll 4
+      for (int e = 4 * threadIdx.x; e < tile; e += 4 * blockDim.x) {
+        float4 re = *reinterpret_cast<const float4*>(in0 + base + e), im = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s0) {  // sub(z1, u1) (admm.cpp:147)
+          const float4 d = *reinterpret_cast<const float4*>(s0 + base + e);
+          re = make_float4(re.x - d.x, re.y - d.y, re.z - d.z, re.w - d.w);
+        }
+        if (in1) {
+          im = *reinterpret_cast<const float4*>(in1 + base + e);
+          if (s1) {
+            const float4 d = *reinterpret_cast<const float4*>(s1 + base + e);
+            im = make_float4(im.x - d.x, im.y - d.y, im.z - d.z, im.w - d.w);
+          }
+        }
+        sm[srow(e, logn)] = {re.x, im.x};
+        sm[srow(e + 1, logn)] = {re.y, im.y};
+        sm[srow(e + 2, logn)] = {re.z, im.z};
+        sm[srow(e + 3, logn)] = {re.w, im.w};
+      }
+      goto loaded;
+    }
+  }
 #pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     R re = ld_r<R>(in0 + base + e), im = R(0);
@@ -168,9 +197,20 @@ __global__ void __launch_bounds__(512, 3) row_fwd_kernel(const T* __restrict__ s
     }
     sm[srow(e, logn)] = {re, im};
   }
+loaded:
   __syncthreads();
   fft_dif_seq(sm, nr, n, logn, tw);
   C* o = out + p * plane + base;
+  if constexpr (std::is_same<R, float>::value) {
+    if (n >= 2) {  // two complex per 16-byte store
+#pragma unroll 4
+      for (int e = 2 * threadIdx.x; e < tile; e += 2 * blockDim.x) {
+        const C u = sm[srow(e, logn)], v = sm[srow(e + 1, logn)];
+        *reinterpret_cast<float4*>(o + e) = make_float4(u.x, u.y, v.x, v.y);
+      }
+      return;
+    }
+  }
 #pragma unroll 8
   for (int e = threadIdx.x; e < tile; e += blockDim.x) o[e] = sm[srow(e, logn)];
 }
@@ -197,8 +237,22 @@ __global__ void __launch_bounds__(512, 3) row_inv_kernel(const typename Cx<R>::T
   const int64_t p = row0 >> logn, lr0 = row0 - (p << logn);
   const int64_t base = lr0 * n;
   const C* src = in + p * plane + base;
+  bool vec = false;
+  if constexpr (std::is_same<R, float>::value) {
+    if (n >= 2) {  // two complex per 16-byte load
+      vec = true;
+#pragma unroll 4
+      for (int e = 2 * threadIdx.x; e < tile; e += 2 * blockDim.x) {
+        const float4 u = *reinterpret_cast<const float4*>(src + e);
+        sm[srow(e, logn)] = {u.x, u.y};
+        sm[srow(e + 1, logn)] = {u.z, u.w};
+      }
+    }
+  }
+  if (!vec) {
 #pragma unroll 8
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[srow(e, logn)] = src[e];
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[srow(e, logn)] = src[e];
+  }
   __syncthreads();
   ifft_dit_seq(sm, nr, n, logn, tw);
   int64_t o0, o1 = -1;  // element offsets of the two output planes
