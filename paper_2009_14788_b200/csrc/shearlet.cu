@@ -284,8 +284,22 @@ __global__ void __launch_bounds__(512, 3) row_inv_kernel(const typename Cx<R>::T
 // staged column-major in shared memory with a padded stride.
 __host__ __device__ inline int col_ld(int n) { return n + 4; }
 
+// (fp32: two adjacent columns per 16-byte access — scratch planes are aligned)
 template <class C>
 __device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int n, int tc, int c0, int ld) {
+  if constexpr (std::is_same<C, float2>::value) {
+    if ((tc & 1) == 0) {
+      const int hp = tc >> 1;
+#pragma unroll 8
+      for (int e = threadIdx.x; e < hp * n; e += blockDim.x) {
+        const int r = e / hp, c = 2 * (e - r * hp);
+        const float4 u = *reinterpret_cast<const float4*>(src + int64_t(r) * n + c0 + c);
+        sm[c * ld + fft_swz(r)] = make_float2(u.x, u.y);
+        sm[(c + 1) * ld + fft_swz(r)] = make_float2(u.z, u.w);
+      }
+      return;
+    }
+  }
 #pragma unroll 8
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
@@ -294,6 +308,18 @@ __device__ __forceinline__ void load_cols(C* sm, const C* __restrict__ src, int 
 }
 template <class C>
 __device__ __forceinline__ void store_cols(C* __restrict__ dst, const C* sm, int n, int tc, int c0, int ld) {
+  if constexpr (std::is_same<C, float2>::value) {
+    if ((tc & 1) == 0) {
+      const int hp = tc >> 1;
+#pragma unroll 8
+      for (int e = threadIdx.x; e < hp * n; e += blockDim.x) {
+        const int r = e / hp, c = 2 * (e - r * hp);
+        const C u = sm[c * ld + fft_swz(r)], v = sm[(c + 1) * ld + fft_swz(r)];
+        *reinterpret_cast<float4*>(dst + int64_t(r) * n + c0 + c) = make_float4(u.x, u.y, v.x, v.y);
+      }
+      return;
+    }
+  }
 #pragma unroll 8
   for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
     const int r = e / tc, c = e - r * tc;
