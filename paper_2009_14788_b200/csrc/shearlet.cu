@@ -349,11 +349,28 @@ __global__ void __launch_bounds__(512, 3) col_kernel(const typename Cx<R>::T* __
     const int64_t q = q0 + p, j = q / B, b = q % B;
     const C* src = in + b * plane;
     const C* mk = mult2 + j * plane;
-  #pragma unroll 8
-    for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
-      const int r = e / tc, c = e - r * tc;
-      const int64_t gi = int64_t(r) * n + c0 + c;
-      sm[c * ld + fft_swz(r)] = cmul(src[gi], mk[gi]);
+    bool done = false;
+    if constexpr (std::is_same<C, float2>::value) {
+      if ((tc & 1) == 0) {  // two adjacent columns per 16-byte load
+        const int hp = tc >> 1;
+#pragma unroll 8
+        for (int e = threadIdx.x; e < hp * n; e += blockDim.x) {
+          const int r = e / hp, c = 2 * (e - r * hp);
+          const int64_t gi = int64_t(r) * n + c0 + c;
+          const float4 x = *reinterpret_cast<const float4*>(src + gi), w = *reinterpret_cast<const float4*>(mk + gi);
+          sm[c * ld + fft_swz(r)] = cmul(make_float2(x.x, x.y), make_float2(w.x, w.y));
+          sm[(c + 1) * ld + fft_swz(r)] = cmul(make_float2(x.z, x.w), make_float2(w.z, w.w));
+        }
+        done = true;
+      }
+    }
+    if (!done) {
+#pragma unroll 8
+      for (int e = threadIdx.x; e < tc * n; e += blockDim.x) {
+        const int r = e / tc, c = e - r * tc;
+        const int64_t gi = int64_t(r) * n + c0 + c;
+        sm[c * ld + fft_swz(r)] = cmul(src[gi], mk[gi]);
+      }
     }
   } else if (mode == 3) {
   #pragma unroll 8
