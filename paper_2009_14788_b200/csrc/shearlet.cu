@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(512, 3) row_fwd_kernel(const T* __restrict__ s
     }
   }
   const int64_t base = lr0 * n;
+  bool loaded = false;
   if constexpr (std::is_same<T, float>::value && std::is_same<R, float>::value) {
     // four reals per 16-byte load (memory-level parallelism: the pass is
     // latency-bound on its global reads); caller buffers may be misaligned
@@ -184,20 +185,21 @@ __global__ void __launch_bounds__(512, 3) row_fwd_kernel(const T* __restrict__ s
         sm[srow(e + 2, logn)] = {re.z, im.z};
         sm[srow(e + 3, logn)] = {re.w, im.w};
       }
-      goto loaded;
+      loaded = true;
     }
   }
+  if (!loaded) {
 #pragma unroll 8
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-    R re = ld_r<R>(in0 + base + e), im = R(0);
-    if (s0) re = re - ld_r<R>(s0 + base + e);  // sub(z1, u1) (admm.cpp:147)
-    if (in1) {
-      im = ld_r<R>(in1 + base + e);
-      if (s1) im = im - ld_r<R>(s1 + base + e);
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+      R re = ld_r<R>(in0 + base + e), im = R(0);
+      if (s0) re = re - ld_r<R>(s0 + base + e);  // sub(z1, u1) (admm.cpp:147)
+      if (in1) {
+        im = ld_r<R>(in1 + base + e);
+        if (s1) im = im - ld_r<R>(s1 + base + e);
+      }
+      sm[srow(e, logn)] = {re, im};
     }
-    sm[srow(e, logn)] = {re, im};
   }
-loaded:
   __syncthreads();
   fft_dif_seq(sm, nr, n, logn, tw);
   C* o = out + p * plane + base;
