@@ -7,14 +7,24 @@
 #include <cstring>
 #include <memory>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "rk_internal.hpp"
 
 namespace {
 
 thread_local std::string g_last_error;
 
+// NVTX range per C-ABI call (header-only NVTX v3: a no-op unless a profiler
+// such as Nsight Systems injects itself), named after the entry point.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <class F>
-int guarded(F&& f) {
+int guarded_named(const char* name, F&& f) {
+  NvtxRange range(name);
   try {
     f();
     return RK_OK;
@@ -183,14 +193,14 @@ const char* rk_last_error(void) { return g_last_error.c_str(); }
 const char* rk_version(void) { return "radon_b200 0.1 (sm_100a)"; }
 
 int rk_geometry_resolve(const rk_geometry* in, rk_geometry* out) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(in != nullptr && out != nullptr, "geometry pointer is null");
     *out = rk::resolve_geometry(*in);
   });
 }
 
 int rk_angles_linspace(double start, double stop, int64_t n, double* out) {
-  return guarded([&] {  // geometry.cpp:67-73
+  return guarded_named(__func__, [&] {  // geometry.cpp:67-73
     if (n < 1) throw rk::ValidationError("angle count must be >= 1, got " + std::to_string(n));
     require(out != nullptr, "output pointer is null");
     double step = (stop - start) / double(n);
@@ -199,7 +209,7 @@ int rk_angles_linspace(double start, double stop, int64_t n, double* out) {
 }
 
 int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(geometry != nullptr && plan != nullptr, "geometry / plan pointer is null");
     *plan = nullptr;
     auto hp = std::make_unique<rk_plan>();
@@ -221,7 +231,7 @@ int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan) {
 }
 
 int rk_plan_destroy(rk_plan* plan) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     if (!plan) return;
     cudaSetDevice(plan->p.device);
     cudaDeviceSynchronize();
@@ -230,7 +240,7 @@ int rk_plan_destroy(rk_plan* plan) {
 }
 
 int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_plan(plan);
     require(info != nullptr, "info pointer is null");
     const rk::Plan& p = plan->p;
@@ -244,7 +254,7 @@ int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info) {
 
 // projector.cpp:228-236 (forward: shape + options checked, output keeps the precision)
 int rk_forward(rk_plan* plan, int dtype, const void* d_image, int64_t batch, void* d_sino, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -257,7 +267,7 @@ int rk_forward(rk_plan* plan, int dtype, const void* d_image, int64_t batch, voi
 
 // projector.cpp:252-260
 int rk_backproject(rk_plan* plan, int dtype, const void* d_sino, int64_t batch, void* d_image, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -269,7 +279,7 @@ int rk_backproject(rk_plan* plan, int dtype, const void* d_sino, int64_t batch, 
 }
 
 int rk_filter_kind_from_name(const char* name, int* kind) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(name != nullptr && kind != nullptr, "name / kind pointer is null");
     *kind = rk::filter_kind_from_name(name);
   });
@@ -278,7 +288,7 @@ int rk_filter_kind_from_name(const char* name, int* kind) {
 const char* rk_filter_kind_name(int kind) { return rk::filter_kind_name(kind); }
 
 int rk_filter_create(int kind, int64_t det_count, int device, rk_filter** filter) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(filter != nullptr, "filter pointer is null");
     *filter = nullptr;
     auto hf = std::make_unique<rk_filter>();
@@ -294,7 +304,7 @@ int rk_filter_create(int kind, int64_t det_count, int device, rk_filter** filter
 }
 
 int rk_filter_destroy(rk_filter* filter) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     if (!filter) return;
     cudaSetDevice(filter->f.device);
     cudaDeviceSynchronize();
@@ -303,7 +313,7 @@ int rk_filter_destroy(rk_filter* filter) {
 }
 
 int rk_filter_response(const rk_filter* filter, int64_t* padded_size, double* response, float* response_f) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(filter != nullptr, "filter is null");
     const rk::Filter& f = filter->f;
     if (padded_size) *padded_size = f.padded;
@@ -315,7 +325,7 @@ int rk_filter_response(const rk_filter* filter, int64_t* padded_size, double* re
 // sino_filter.cpp:98-104 (3-D shape, det_count must match the filter)
 int rk_filter_sinogram(rk_filter* filter, int dtype, const void* d_in, int64_t batch, int64_t n_angles,
                        void* d_out, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_filter(filter);
     check_dtype(dtype);
     require(batch >= 1 && n_angles >= 1, "sinogram must have batch >= 1 and n_angles >= 1");
@@ -330,7 +340,7 @@ int rk_filter_sinogram(rk_filter* filter, int dtype, const void* d_in, int64_t b
 // sino_filter.cpp:126-136
 int rk_fbp(rk_plan* plan, rk_filter* filter, int dtype, const void* d_sino, int64_t batch, void* d_image,
            void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_device_filter(filter);
     check_dtype(dtype);
@@ -346,7 +356,7 @@ int rk_fbp(rk_plan* plan, rk_filter* filter, int dtype, const void* d_sino, int6
 }
 
 int rk_forward_host(rk_plan* plan, int dtype, const void* h_image, int64_t batch, void* h_sino) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -361,7 +371,7 @@ int rk_forward_host(rk_plan* plan, int dtype, const void* h_image, int64_t batch
 }
 
 int rk_backproject_host(rk_plan* plan, int dtype, const void* h_sino, int64_t batch, void* h_image) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -377,7 +387,7 @@ int rk_backproject_host(rk_plan* plan, int dtype, const void* h_sino, int64_t ba
 
 int rk_filter_sinogram_host(rk_filter* filter, int dtype, const void* h_in, int64_t batch, int64_t n_angles,
                             void* h_out) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_filter(filter);
     check_dtype(dtype);
     require(batch >= 1 && n_angles >= 1, "sinogram must have batch >= 1 and n_angles >= 1");
@@ -396,7 +406,7 @@ int rk_filter_sinogram_host(rk_filter* filter, int dtype, const void* h_in, int6
 }
 
 int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino, int64_t batch, void* h_image) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_device_filter(filter);
     check_dtype(dtype);
@@ -415,7 +425,7 @@ int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino,
 
 // solvers.cpp:111-128
 int rk_estimate_alpha(rk_plan* plan, int iterations, uint64_t seed, double* alpha) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     require(alpha != nullptr, "alpha pointer is null");
     rk::Plan& p = plan->p;
@@ -428,7 +438,7 @@ int rk_estimate_alpha(rk_plan* plan, int iterations, uint64_t seed, double* alph
 // solvers.cpp:130-145
 int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, double alpha,
                  int iterations, void* d_x, int* failed_iteration, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -449,7 +459,7 @@ int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess,
 // solvers.cpp:162-166 (cg_impl :47-107)
 int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int64_t batch, int max_iter,
             double tolerance, void* d_x, int* failed_iteration, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     check_device_plan(plan);
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -468,7 +478,7 @@ int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int6
 
 int rk_shearlet_create(int64_t height, int64_t width, const double* alphas, int n_scales, int device,
                        rk_shearlet** plan) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(plan != nullptr, "plan pointer is null");
     require(alphas != nullptr || n_scales == 0, "alphas pointer is null");
     *plan = nullptr;
@@ -486,7 +496,7 @@ int rk_shearlet_create(int64_t height, int64_t width, const double* alphas, int 
 
 int rk_shearlet_create_stored(int64_t height, int64_t width, const double* alphas, int n_scales,
                               const double* multipliers, int device, rk_shearlet** plan) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(plan != nullptr, "plan pointer is null");
     require(alphas != nullptr || n_scales == 0, "alphas pointer is null");
     require(multipliers != nullptr, "multipliers pointer is null");
@@ -505,7 +515,7 @@ int rk_shearlet_create_stored(int64_t height, int64_t width, const double* alpha
 }
 
 int rk_shearlet_destroy(rk_shearlet* plan) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     if (!plan) return;
     if (plan->s.device >= 0) {
       cudaSetDevice(plan->s.device);
@@ -516,7 +526,7 @@ int rk_shearlet_destroy(rk_shearlet* plan) {
 }
 
 int rk_shearlet_info(const rk_shearlet* plan, int64_t* n_coeff, double* scales, double* multipliers) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(plan != nullptr, "plan is null");
     const rk::Shearlet& s = plan->s;
     if (n_coeff) *n_coeff = s.n_coeff;
@@ -528,7 +538,7 @@ int rk_shearlet_info(const rk_shearlet* plan, int64_t* n_coeff, double* scales, 
 // shearlet.cpp:296-311
 int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64_t batch, void* d_coeff,
                         void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(plan != nullptr && plan->s.device >= 0, "shearlet plan is null or host-only");
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -542,7 +552,7 @@ int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64
 // shearlet.cpp:313-330
 int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int64_t batch, void* d_image,
                          void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(plan != nullptr && plan->s.device >= 0, "shearlet plan is null or host-only");
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
@@ -590,7 +600,7 @@ struct rk_admm_state {
 
 int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0,
                    double p1, const double* weights, int inner_cg_iterations, void* stream, rk_admm_state** out) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(out != nullptr, "admm pointer is null");
     *out = nullptr;
     check_admm_args(plan, shearlet, dtype, batch, p0, p1);
@@ -615,7 +625,7 @@ int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* 
 }
 
 int rk_admm_iterate(rk_admm_state* admm, int64_t n, int64_t* failed_iteration, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(admm != nullptr, "admm is null");
     if (n < 0) throw rk::ValidationError("admm outer_iterations must be nonnegative");
     rk::Admm& a = admm->a;
@@ -632,7 +642,7 @@ int rk_admm_iterate(rk_admm_state* admm, int64_t n, int64_t* failed_iteration, v
 }
 
 int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* stream) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(admm != nullptr, "admm is null");
     require(d_dst != nullptr, "destination pointer is null");
     check_dtype(dtype);
@@ -644,7 +654,7 @@ int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* s
 }
 
 int rk_admm_destroy(rk_admm_state* admm) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     if (!admm) return;
     cudaSetDevice(admm->a.plan->device);
     cudaDeviceSynchronize();
@@ -672,18 +682,18 @@ int rk_admm(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino,
 }
 
 int rk_profiling_enable(int enable) {
-  return guarded([&] { rk::profiling_enable(enable != 0); });
+  return guarded_named(__func__, [&] { rk::profiling_enable(enable != 0); });
 }
 
 int rk_profiling_read(rk_kernel_stats* stats, int reset) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(stats != nullptr, "stats pointer is null");
     rk::profiling_read(stats, reset != 0);
   });
 }
 
 int rk_probe_smem_bandwidth(int device, double* gbs) {
-  return guarded([&] {
+  return guarded_named(__func__, [&] {
     require(gbs != nullptr, "output pointer is null");
     *gbs = rk::probe_smem_bandwidth(device);
   });
