@@ -417,7 +417,26 @@ def measure_extras(rk, _lib, dev):
     ms = timed(lambda: rk.backprojection(gf, rk.forward(gf, x)))
     out["cfg3_fan512_b128_fp32"] = {"metric": "forward+backprojection images/s", "value": 128 / (ms * 1e-3),
                                     "ms": ms}
-    del x, y
+    # the same through the host-buffer entry points (pinned buffers, copies inside), wall clock
+    pf = rk.get_plan(gf, None, dev.index or 0)
+    h_img = x.cpu().pin_memory()
+    h_sino, h_out = torch.empty(tuple(y.shape)).pin_memory(), torch.empty(tuple(x.shape)).pin_memory()
+
+    def host_pair():
+        _lib.check(_lib.lib.rk_forward_host(pf.handle, _lib.RK_F32, ctypes_void(h_img.data_ptr()), 128,
+                                            ctypes_void(h_sino.data_ptr())))
+        _lib.check(_lib.lib.rk_backproject_host(pf.handle, _lib.RK_F32, ctypes_void(h_sino.data_ptr()), 128,
+                                                ctypes_void(h_out.data_ptr())))
+
+    host_pair()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        host_pair()
+    el = (time.perf_counter() - t0) / 3
+    out["cfg3_fan512_b128_fp32"]["e2e"] = {"value": 128 / el, "unit": "images/s", "ms": 1e3 * el,
+                                           "h2d_bytes_per_step": h_img.numel() * 4 + h_sino.numel() * 4,
+                                           "d2h_bytes_per_step": h_sino.numel() * 4 + h_out.numel() * 4}
+    del x, y, h_img, h_sino, h_out
     # config 4: FBP 1024^2, 720 angles, nd 1024 and 1449, batch 64, fp32 and fp16 storage
     ph = rk_phantom(1024)
     x = torch.from_numpy(np.stack([ph * ((e + 1) / 64.0) for e in range(64)])).to(dev)
