@@ -25,6 +25,7 @@
 //     exact fp64 ray segments with one unit of slack in t and one texel around
 //     the taps (the kernel assigns samples to chunks in fp32).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -69,8 +70,14 @@ void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, doubl
         ++used;
       }
       if (!used) continue;
+      // A tap offset applied to every lane shifts every slot by the same amount,
+      // which leaves the conflicts unchanged: with no swap all four taps cost
+      // what tap 0 costs; with a row (column) swap only the row (column) bit of
+      // the tap matters.  So 5 of the 12 (swap, tap) patterns are evaluated.
       for (int sw = 0; sw < 3; ++sw)
         for (int tap = 0; tap < 4; ++tap) {
+          const int weight = sw == 0 ? (tap == 0 ? 4 : 0) : sw == 1 ? ((tap & 1) ? 0 : 2) : ((tap & 2) ? 0 : 2);
+          if (!weight) continue;
           int64_t ti[8], tj[8];
           bool first[8];
           for (int u = 0; u < used; ++u) {
@@ -86,7 +93,7 @@ void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, doubl
             int worst = 1;
             for (int u = 0; u < used; ++u)
               if (first[u]) worst = std::max(worst, ++cnt[int((((ti[u] * pitch + tj[u]) % 8) + 8) % 8)]);
-            cost[sw][r] += worst;
+            cost[sw][r] += weight * worst;
           }
         }
     }
@@ -433,15 +440,19 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     std::vector<int2> warps = warps_of(sh);
     const int ctas = int(warps.size() / 8);
     plans.assign(size_t(ctas), CtaPlan{});
-    auto work = [&](int lo, int hi) {
+    std::atomic<int> next{0};  // CTAs differ in work (ray lengths): hand them out in small blocks
+    auto work = [&]() {
       std::vector<Pt> sim;
-      for (int cta = lo; cta < hi; ++cta)
-        plan_cta(&warps[size_t(cta) * 8], sh.aa == 8 && sh.db == 1, plans[size_t(cta)], sim);
+      for (int lo; (lo = next.fetch_add(4)) < ctas;)
+        for (int cta = lo; cta < std::min(lo + 4, ctas); ++cta)
+          plan_cta(&warps[size_t(cta) * 8], sh.aa == 8 && sh.db == 1, plans[size_t(cta)], sim);
     };
-    const int nthreads = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), ctas));
+    const char* pte = std::getenv("RK_PLAN_THREADS");  // planner threads (default: all host threads)
+    const int want = pte ? std::atoi(pte) : int(std::thread::hardware_concurrency());
+    const int nthreads = std::max(1, std::min<int>(want, ctas));
     std::vector<std::thread> pool;
     for (int t = 0; t < nthreads; ++t)
-      pool.emplace_back(work, int(int64_t(ctas) * t / nthreads), int(int64_t(ctas) * (t + 1) / nthreads));
+      pool.emplace_back(work);
     for (auto& th : pool) th.join();
     return warps;
   };
