@@ -50,6 +50,17 @@ WORKLOADS = {
 }
 
 
+def hbm_check(traffic_bytes, ms):
+    """The dominant kernel's measured DRAM traffic (ncu, per launch) over its event-timed duration,
+    against the driver-measured HBM copy bandwidth (MEASURED_PEAKS.json)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if traffic_bytes is None or not os.path.exists(path) or not ms or ms != ms:
+        return None
+    peak = float(json.load(open(path))["hbm_gbs"])
+    gbs = traffic_bytes / (ms * 1e-3) / 1e9
+    return {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "peak_source": "MEASURED_PEAKS.json"}
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -321,6 +332,11 @@ def main():
                                 "HBM is not the binding resource: the kernel's data path is shared memory",
                 "peak_source": "measured in this run by rk_probe_smem_bandwidth (LDS.128, all SMs); "
                                "MEASURED_PEAKS.json has no L1TEX/SMEM figure",
+                "peak_nominal": 148 * 128 * 1.965,  # SMs x 128 B/clk (one LDS wavefront) x max SM clock, GB/s
+                "bound_note": "neither HBM nor the tensor cores bind this gather kernel (SURVEY 8d): its "
+                              "algorithmic unit is the shared-memory tap read, so the peak is the L1TEX/SMEM "
+                              "bandwidth; the HBM check below uses MEASURED_PEAKS.json",
+                "hbm_check": hbm_check(traffic, dms),
                 "algorithmic_bytes_per_launch": dbytes,
                 "per_kernel": {
                     "forward": {"samples_per_launch": info["forward_samples"] * nb, "bytes_per_sample": 16,
