@@ -15,6 +15,7 @@ from __future__ import annotations
 import argparse
 import json
 import math
+import os
 import sys
 import time
 
@@ -121,6 +122,8 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2009_14788_b200", description=__doc__.split("\n")[0])
     ap.add_argument("--json", action="store_true", help="emit reports as JSON on stdout")
     ap.add_argument("--version", action="version", version=VERSION)
+    ap.add_argument("--threads", type=int, default=0,
+                    help="cap host worker threads (planner, host copies; 0: hardware default); results do not change")
     sub = ap.add_subparsers(dest="cmd", required=True)
     p = sub.add_parser("project", help="forward-project an image to a sinogram")
     _geo_args(p)
@@ -158,10 +161,13 @@ def main(argv=None) -> int:
     p.add_argument("-o", "--out", required=True)
     p.add_argument("--reference", default="")
     p.add_argument("--precision", choices=list(_PREC), default="")
-    p = sub.add_parser("check-adjoint", help="dot-product test of the projector pair")
+    p = sub.add_parser("check-adjoint", help="dot-product test of an operator pair")
     _geo_args(p)
+    p.add_argument("--operator", dest="op_name", default="projector", choices=["projector", "shearlet"])
     p.add_argument("--size", type=int, default=64)
-    p.add_argument("--trials", type=int, default=8)
+    p.add_argument("--scales", type=int, default=5, help="shearlet scales")
+    p.add_argument("--alpha", type=float, default=0.5, help="shearlet scaling exponent")
+    p.add_argument("--trials", type=int, default=10)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--tolerance", type=float, default=0.0)
     p = sub.add_parser("bench", help="time forward and backprojection throughput")
@@ -196,7 +202,17 @@ def main(argv=None) -> int:
     p.add_argument("--progress", action="store_true", help="print the objective each outer iteration to stderr")
     p.add_argument("--cache-dir", default="")
     p.add_argument("--reference", default="")
-    a = ap.parse_args(argv)
+    try:
+        a = ap.parse_args(argv)
+    except SystemExit as e:  # usage errors exit 1, --help / --version 0 (cli.cpp:711-716)
+        return 0 if e.code in (0, None) else 1
+    if a.threads > 0:  # cli.cpp:719 set_num_threads: the host-side workers here
+        import os
+
+        import torch
+
+        os.environ["RK_PLAN_THREADS"] = str(a.threads)
+        torch.set_num_threads(a.threads)
     try:
         return _run(rk, a)
     except ValidationError as e:
@@ -205,6 +221,9 @@ def main(argv=None) -> int:
     except NumericalError as e:
         print(f"numerical error: {e}", file=sys.stderr)
         return 2
+    except Exception as e:  # noqa: BLE001 — any other failure (missing file, I/O): exit 1 like cli.cpp:727-729
+        print(f"error: {e}", file=sys.stderr)
+        return 1
 
 
 def _run(rk, a) -> int:
@@ -276,16 +295,27 @@ def _run(rk, a) -> int:
             print(json.dumps(rep, indent=2))
         return 0
     if a.cmd == "check-adjoint":  # cli.cpp:581-616
-        g = build_geometry(a, a.size, a.angles if a.angles > 0 else a.size)
-        d = rk.adjoint_check(rk.projector_operator(g, rk.ProjectorOptions(a.step)), a.trials, a.seed)
+        if a.trials < 1:
+            raise ValidationError("--trials must be positive")
+        if a.op_name == "shearlet":
+            plan = rk.make_plan(a.size, a.size, [a.alpha] * a.scales)
+            op = rk.shearlet_operator(plan)
+            detail = {"size": a.size, "scales": a.scales, "alpha": a.alpha, "n_coeff": plan.n_coeff}
+            line = f"size={a.size} scales={a.scales}"
+        else:
+            g = build_geometry(a, a.size, a.angles if a.angles > 0 else a.size)
+            op = rk.projector_operator(g, rk.ProjectorOptions(a.step))
+            detail = geometry_json(g)
+            line = f"{g.__class__.__name__} size={a.size}"
+        d = rk.adjoint_check(op, a.trials, a.seed)
         if a.json:
-            rep = {"command": "check-adjoint", "operator": "projector", "defect": d, "trials": a.trials,
-                   "seed": a.seed, "detail": geometry_json(g)}
+            rep = {"command": "check-adjoint", "operator": a.op_name, "defect": d, "trials": a.trials,
+                   "seed": a.seed, "detail": detail}
             if a.tolerance > 0:
                 rep["tolerance"] = a.tolerance
             print(json.dumps(rep, indent=2))
         else:
-            print(f"adjoint defect: {d:.6e}")
+            print(f"adjoint defect: {d:.6e} ({a.op_name} {line} trials={a.trials} seed={a.seed})")
         if a.tolerance > 0 and not (d <= a.tolerance):
             print(f"adjoint defect {d:.6e} exceeds tolerance {a.tolerance:.6e}", file=sys.stderr)
             return 2
@@ -318,7 +348,8 @@ def _run(rk, a) -> int:
         fwd = time_op(lambda: rk.forward(g, img, opts))
         bwd = time_op(lambda: rk.backprojection(g, sino, opts))
         rep = {"version": VERSION, "geometry": geometry_json(g), "batch": a.batch, "precision": a.precision,
-               "warmup": a.warmup, "runs": a.runs, "threads": 1, "device": torch.cuda.get_device_name(),
+               "warmup": a.warmup, "runs": a.runs, "threads": a.threads if a.threads > 0 else (os.cpu_count() or 1),
+               "device": torch.cuda.get_device_name(),
                "forward": fwd, "backprojection": bwd}
         if a.json:
             print(json.dumps(rep, indent=2))

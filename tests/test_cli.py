@@ -123,3 +123,85 @@ def test_cli_shearlet_and_admm(tmp_path, ref, cuda):
     rep = json.loads(r.stdout)
     assert rep["command"] == "admm" and rep["outer"] == 20 and rep["mse_vs_reference"] < 1.5e-2
     assert rep["geometry"]["n_angles"] == 32
+
+
+def test_cli_usage_and_io_errors_exit_1(tmp_path):
+    """test_cli.cpp:197-200: unknown flags and unreadable inputs exit 1 (cli.cpp:711-729)."""
+    assert cli("--no-such-flag").returncode == 1
+    assert cli("project", "--in", str(tmp_path / "absent.npy"), "-o", str(tmp_path / "x.npy")).returncode == 1
+    assert cli("--version").returncode == 0
+
+
+@pytest.mark.gpu
+def test_cli_solve_methods_reconstruct_and_report(tmp_path, cuda):
+    """test_cli.cpp:111-140.  cg runs the generic CG on the normal equations and
+    cgne the fused device CGNE: the same algorithm, equal to fp32 rounding (the
+    reference's two paths share one implementation and agree bitwise)."""
+    assert cli("phantom", "--size", "32", "-o", str(tmp_path / "ph.npy")).returncode == 0
+    assert cli("project", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "sino.npy"), "--angles",
+               "45").returncode == 0
+
+    def solve(method, out):
+        r = cli("--json", "solve", "--method", method, "--iterations", "30", "--size", "32", "--angles", "45",
+                "--in", str(tmp_path / "sino.npy"), "-o", str(tmp_path / out), "--reference", str(tmp_path / "ph.npy"))
+        assert r.returncode == 0, r.stderr
+        return json.loads(r.stdout)
+
+    jl = solve("landweber", "lw.npy")
+    assert jl["method"] == "landweber" and jl["alpha"] > 0.0 and jl["mse_vs_reference"] < 2e-2
+    assert solve("cg", "cg.npy")["mse_vs_reference"] < 1e-2
+    assert solve("cgne", "cgne.npy")["mse_vs_reference"] < 1e-2
+    a, b = np.load(tmp_path / "cg.npy"), np.load(tmp_path / "cgne.npy")
+    assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
+
+
+@pytest.mark.gpu
+def test_cli_check_adjoint_tolerance_and_operators(cuda):
+    """test_cli.cpp:161-176."""
+    assert cli("check-adjoint", "--size", "32", "--trials", "5", "--tolerance", "2e-2").returncode == 0
+    assert cli("check-adjoint", "--size", "32", "--trials", "5", "--tolerance", "1e-9").returncode == 2
+    assert cli("check-adjoint", "--operator", "shearlet", "--size", "32", "--scales", "3", "--tolerance",
+               "1e-4").returncode == 0
+    r = cli("--json", "check-adjoint", "--size", "32", "--trials", "5")
+    assert r.returncode == 0
+    j = json.loads(r.stdout)
+    assert j["operator"] == "projector" and j["trials"] == 5 and 0.0 < j["defect"] < 2e-2
+
+
+@pytest.mark.gpu
+def test_cli_numerical_and_validation_exit_codes(tmp_path, cuda):
+    """test_cli.cpp:197-214: fan source inside the image -> 1; a diverging Landweber step -> 2."""
+    assert cli("phantom", "--size", "32", "-o", str(tmp_path / "ph.npy")).returncode == 0
+    assert cli("project", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "sino.npy"), "--angles",
+               "45").returncode == 0
+    assert cli("backproject", "--size", "512", "--geometry", "fanbeam", "--source-distance", "300", "--in",
+               str(tmp_path / "sino.npy"), "-o", str(tmp_path / "x.npy")).returncode == 1
+    assert cli("solve", "--method", "landweber", "--alpha", "1.0", "--iterations", "60", "--size", "32", "--angles",
+               "45", "--in", str(tmp_path / "sino.npy"), "-o", str(tmp_path / "x.npy")).returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_thread_cap_half_and_ranks(tmp_path, cuda):
+    """test_cli.cpp:216-251: --threads does not change results; half precision
+    flows end to end; 2-d and batched 3-d files give the same bytes."""
+    assert cli("phantom", "--size", "32", "-o", str(tmp_path / "ph.npy")).returncode == 0
+    assert cli("--threads", "1", "project", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "s1.npy")).returncode == 0
+    assert cli("--threads", "3", "project", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "s3.npy")).returncode == 0
+    assert (tmp_path / "s1.npy").read_bytes() == (tmp_path / "s3.npy").read_bytes()
+
+    assert cli("phantom", "--size", "32", "-o", str(tmp_path / "ph16.npy"), "--precision", "half").returncode == 0
+    assert np.load(tmp_path / "ph16.npy").dtype == np.float16
+    assert cli("project", "--in", str(tmp_path / "ph16.npy"), "-o", str(tmp_path / "s16.npy")).returncode == 0
+    assert np.load(tmp_path / "s16.npy").dtype == np.float16
+    assert cli("fbp", "--size", "32", "--in", str(tmp_path / "s16.npy"), "-o", str(tmp_path / "rec.npy"), "--precision",
+               "single").returncode == 0
+    assert np.load(tmp_path / "rec.npy").dtype == np.float32
+
+    assert cli("project", "--in", str(tmp_path / "ph.npy"), "-o", str(tmp_path / "sino2d.npy"), "--angles",
+               "24").returncode == 0
+    s2 = np.load(tmp_path / "sino2d.npy")
+    np.save(tmp_path / "sino3d.npy", s2[None])
+    for name in ("2", "3"):
+        assert cli("backproject", "--size", "32", "--in", str(tmp_path / f"sino{name}d.npy"), "-o",
+                   str(tmp_path / f"b{name}.npy")).returncode == 0
+    assert (tmp_path / "b2.npy").read_bytes() == (tmp_path / "b3.npy").read_bytes()
