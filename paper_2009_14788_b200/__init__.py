@@ -22,6 +22,7 @@ from .solvers import cg, cgne, estimate_alpha, landweber
 from . import shearlet
 from .shearlet import ShearletPlan, backward, make_plan, make_plan_cached, shearlet_operator
 from .admm import AdmmParams, AdmmState, admm_objective, admm_reconstruct, default_weights, shrink
+from .npy import read_array, write_array
 
 
 def forward(plan_or_geometry, x, *args, **kwargs):
@@ -42,4 +43,5 @@ __all__ = [
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
     "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",
     "AdmmParams", "AdmmState", "admm_objective", "admm_reconstruct", "default_weights", "shrink",
+    "read_array", "write_array",
 ]

@@ -31,7 +31,7 @@ def shepp_logan(s, dtype=np.float32):
     i1 = np.minimum(i0 + 1, base - 1)
     top = (1 - f)[None, :] * img[i0][:, i0] + f[None, :] * img[i0][:, i1]
     bot = (1 - f)[None, :] * img[i1][:, i0] + f[None, :] * img[i1][:, i1]
-    out = (1 - f)[:, None] * top + f[:, None] * bot
+    out = np.ascontiguousarray((1 - f)[:, None] * top + f[:, None] * bot)  # row-major, like Tensor
     dtype = np.dtype(dtype)
     if dtype == np.float64:
         return out

@@ -26,6 +26,7 @@ from . import _arrays as A
 from . import _lib
 from .errors import CudaError, ValidationError
 from .linop import LinearOperator
+from .npy import read_array, write_array
 
 
 def _validate_config(height: int, width: int, alphas) -> None:
@@ -146,14 +147,14 @@ def make_plan_cached(height: int, width: int, alphas, cache_dir: str = "", devic
     n_coeff = 1 + sum(2 * (2 * kj + 1) for kj in k)
     if os.path.exists(path):
         try:
-            stored = np.load(path, allow_pickle=False)
+            stored = read_array(path)
             if stored.dtype == np.float64 and stored.shape == (n_coeff, int(height), int(width)):
                 return _create(height, width, alphas, stored, dev)
-        except (ValueError, OSError):
+        except ValidationError:
             pass  # corrupt entry: rebuild (shearlet.cpp:238-242)
     plan = make_plan(height, width, alphas, dev)
     os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
-    np.save(path, plan.multipliers)
+    write_array(path, plan.multipliers)  # atomic, like the reference's cache write
     return plan
 
 
