@@ -5,6 +5,8 @@ a19; pinned bit-for-bit against the reference by tests/test_oracle_cpu.py).
 """
 import numpy as np
 
+from .errors import ValidationError
+
 _SL = [(1.0, 0.69, 0.92, 0.0, 0.0, 0.0), (-0.8, 0.6624, 0.874, 0.0, -0.0184, 0.0),
        (-0.2, 0.11, 0.31, 0.22, 0.0, -18.0), (-0.2, 0.16, 0.41, -0.22, 0.0, 18.0),
        (0.1, 0.21, 0.25, 0.0, 0.35, 0.0), (0.1, 0.046, 0.046, 0.0, 0.1, 0.0), (0.1, 0.046, 0.046, 0.0, -0.1, 0.0),
@@ -16,6 +18,8 @@ def shepp_logan(s, dtype=np.float32):
     """Synthetic input: modified Shepp-Logan (the reference's table, phantom.cpp:18-29)
     rasterised at 400^2 and bilinearly resampled to s^2 (phantom.cpp:61-101), numpy;
     computed in double and narrowed like Tensor::from_double_as (half via float)."""
+    if int(s) < 1:  # phantom.cpp:62-63
+        raise ValidationError(f"shepp_logan size must be positive, got {s}")
     base = 400
     y = (base - 1 - 2 * np.arange(base))[:, None] / base
     x = (2 * np.arange(base) + 1 - base)[None, :] / base
