@@ -480,15 +480,19 @@ constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 // H8 (fp16 storage, batch > 1): half8 cells, eight images per pixel, 512
 // threads x 2 pixels (the accumulators of eight images), each tap load
 // converted to fp32 pairs; per image the same operations and order.
-template <int KIND, class TOut, bool LANE, bool H8 = false>
-__global__ void __launch_bounds__((LANE || H8) ? 512 : kBpThreads, (LANE || H8) ? 2 : (KIND == kBpFan64 ? 3 : 4))
+// WIDE (small batches, float4 cells): 512 threads x 2 pixels per tile, so the
+// few tiles of one or two image groups still fill the SMs with warps; per pixel
+// the operations and their order are the 256-thread kernel's (bit-identical).
+template <int KIND, class TOut, bool LANE, bool H8 = false, bool WIDE = false>
+__global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
+                                  (LANE || H8 || WIDE) ? 2 : (KIND == kBpFan64 ? 3 : 4))
     backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
     int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
   using Cell = typename std::conditional<LANE, float, float4>::type;
-  constexpr int RPT = (LANE || H8) ? 2 : kRowsPerThread;  // pixels (rows) per thread
+  constexpr int RPT = (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
   constexpr int NT = kTile * kTile / RPT;         // threads
   extern __shared__ float4 smem_raw[];
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
@@ -778,6 +782,15 @@ static bool single_lane(int64_t batch) {
   return on && batch == 1;
 }
 
+// backprojection of at most kWideGroups packed groups: the 512-thread variant
+static bool wide_bp(int64_t groups) {
+  static const int limit = [] {
+    const char* e = std::getenv("RK_BP_WIDE_GROUPS");
+    return e ? std::atoi(e) : 1;
+  }();
+  return groups <= limit;
+}
+
 void launch_forward(const Plan& p, const float4* packed_image, const float4* packed_image_t, int64_t batch,
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
   const ForwardSchedule& F = p.fwd;
@@ -806,7 +819,8 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
   const bool h8 = epi.mode == kOutUser && use_h8(dtype, batch);
   dim3 grid(tiles, tiles, unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
   const bool lane = single_lane(batch);
-  dim3 block(kTile, kTile / ((lane || h8) ? 2 : kRowsPerThread));
+  const bool wide = !lane && !h8 && wide_bp(groups_of(batch));
+  dim3 block(kTile, kTile / ((lane || h8 || wide) ? 2 : kRowsPerThread));
   const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
   const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
   const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
@@ -818,6 +832,10 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                      : (kind == kBpParallel ? backproject_kernel<kBpParallel, T, false>
                         : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false>
                                             : backproject_kernel<kBpFan64, T, false>);
+    if (wide)
+      kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, false, true>
+             : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, false, true>
+                                 : backproject_kernel<kBpFan64, T, false, false, true>;
     if constexpr (std::is_same<T, __half>::value)
       if (h8)
         kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, true>

@@ -301,3 +301,19 @@ def test_large_batch_shards_equal(rk, oracle, cuda):
     bf = rk.backprojection(g, full)
     bp = torch.cat([rk.backprojection(g, full[:6]), rk.backprojection(g, full[6:])])
     assert torch.equal(bf, bp)
+
+
+@pytest.mark.parametrize("name,mk", [("par", lambda rk: par(rk, 100, 37, 77, 1.3)),
+                                     ("fan", lambda rk: fan(rk, 96, 40, 150.0)),
+                                     ("fan-close", lambda rk: fan(rk, 64, 48, 50.0, det_distance=200.0))])
+def test_small_batch_wide_backprojection_equals_batched_bitwise(rk, oracle, cuda, name, mk):
+    """Batches of one packed group run the 512-thread backprojector (kernels.cu WIDE); per
+    pixel it is the 256-thread kernel's arithmetic, so a 4-image call equals the first four
+    images of a 12-image call bit for bit (and matches the oracle)."""
+    g = mk(rk)
+    rs = np.random.default_rng(11)
+    y = rs.standard_normal((12, g.n_angles, g.det_count)).astype(np.float32)
+    full = rk.backprojection(g, dev(y, cuda))
+    small = rk.backprojection(g, dev(y[:4], cuda))
+    assert torch.equal(small, full[:4])
+    assert rel_l2(host(small), oracle.backprojection(ogeom(g), y[:4])) <= TOL32
