@@ -539,6 +539,34 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       F.staged_texels += cp.staged;
       F.any_transposed |= cp.any_tr;
     }
+    // Launch order: longest CTAs first (a warp iterates as long as its longest
+    // ray), so the hardware's in-order CTA dispatch packs the short ones into
+    // the last wave (longest-processing-time list scheduling).  Only the order
+    // of independent CTAs changes — every ray's arithmetic is the same.
+    if (const char* oe = std::getenv("RK_FWD_ORDER"); !(oe && oe[0] == '0')) {
+      const size_t nc = F.cta.size();
+      std::vector<int64_t> work(nc, 0);
+      for (size_t c = 0; c < nc; ++c)
+        for (int w = 0; w < 8; ++w) {
+          const int2 wa = F.warps[c * 8 + size_t(w)];
+          if (wa.x < 0) continue;
+          int64_t longest = 0;
+          for (int l = 0; l < 32 && int64_t(wa.y) + l < nd; ++l)
+            longest = std::max(longest, rays[size_t(int64_t(wa.x) * nd + wa.y + l)].n);
+          work[c] += longest;
+        }
+      std::vector<size_t> idx(nc);
+      for (size_t c = 0; c < nc; ++c) idx[c] = c;
+      std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
+      std::vector<int4> cta2(nc);
+      std::vector<int2> warps2(F.warps.size());
+      for (size_t c = 0; c < nc; ++c) {
+        cta2[c] = F.cta[idx[c]];
+        std::copy_n(F.warps.begin() + int64_t(idx[c] * 8), 8, warps2.begin() + int64_t(c * 8));
+      }
+      F.cta = std::move(cta2);
+      F.warps = std::move(warps2);
+    }
     if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
     if (std::getenv("RK_DEBUG_PLAN")) {
       int64_t ntr = 0;
