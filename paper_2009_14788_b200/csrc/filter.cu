@@ -139,7 +139,7 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
     auto kern = packed_out ? filter_kernel<T, T, 1> : filter_kernel<T, T, 0>;
     if constexpr (std::is_same<T, __half>::value)
       if (packed_out && use_h8(dtype, batch)) kern = filter_kernel<T, T, 2>;
-    if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FILTER, st);
     kern<<<grid, kFilterThreads, smem, st>>>(static_cast<const T*>(in), batch, int(n_angles), int(f.det_count), P,
                                              logP, f.d_response.as<float>(), f.d_twiddle.as<float2>(), scale,

@@ -803,7 +803,7 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
     if constexpr (std::is_same<T, __half>::value)
       if (h8) kern = forward_kernel<T, false, true>;
     const size_t smem = size_t(F.max_box) * (lane ? 2 * sizeof(float) : sizeof(float4));
-    if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FORWARD, st);
     kern<<<grid, kFwdThreads, smem, st>>>(packed_image, packed_image_t, int(p.s), p.ray_geom.as<float4>(),
                                          p.ray_aux.as<float4>(), p.fwd_boxes.as<int4>(), p.fwd_cta.as<int4>(),
@@ -841,7 +841,7 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
         kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, true>
                : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, true>
                                    : backproject_kernel<kBpFan64, T, false, true>;
-    if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
                                     p.g.source_distance, p.g.det_distance, p.trig.as<double2>(),

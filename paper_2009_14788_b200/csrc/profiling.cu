@@ -4,6 +4,7 @@
 // denominators) without a profiler.  Also a shared-memory bandwidth probe —
 // the L1TEX/SMEM roofline peak the projector kernels are bound by.
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -58,6 +59,19 @@ KernelTimer::~KernelTimer() {
 }
 
 void profiling_enable(bool on) { g_timing.store(on); }
+
+void allow_dynamic_smem(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> caps;
+  int dev = 0;
+  RK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cap = caps[{func, dev}];
+  if (bytes <= cap) return;
+  RK_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  cap = bytes;
+}
 
 void profiling_read(rk_kernel_stats* out, bool reset) {
   std::lock_guard<std::mutex> lock(g_mu);

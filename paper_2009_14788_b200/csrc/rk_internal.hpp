@@ -305,6 +305,11 @@ class KernelTimer {
   cudaEvent_t start_ = nullptr, stop_ = nullptr;
   bool active_ = false;
 };
+// Raises a kernel's dynamic shared-memory cap to at least `bytes` (> 48 KB
+// needs the opt-in).  The cap is a process-wide attribute of the function,
+// so it only ever grows: a call needing less never lowers it under a
+// concurrent launch that needs more (calls from several host threads).
+void allow_dynamic_smem(const void* func, size_t bytes);
 void profiling_enable(bool on);
 void profiling_read(rk_kernel_stats* out, bool reset);
 double probe_smem_bandwidth(int device);

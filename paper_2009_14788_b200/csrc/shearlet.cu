@@ -481,7 +481,7 @@ Launch launch_cfg(int n) {
 
 template <class K>
 void smem_opt_in(K kernel, size_t smem) {
-  if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  allow_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
 }
 
 template <class R>

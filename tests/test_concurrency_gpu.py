@@ -13,8 +13,12 @@ pytestmark = pytest.mark.gpu
 
 
 def _geoms(rk):
+    # plans of different sizes need different dynamic shared memory for the same
+    # kernels: the per-function cap must never be lowered under another thread
     return [rk.make_parallel(96, rk.angles_linspace(0.0, np.pi, 72)),
-            rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * np.pi, 64), 150.0)]
+            rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * np.pi, 64), 150.0),
+            rk.make_parallel(256, rk.angles_linspace(0.0, np.pi, 48)),
+            rk.make_fanbeam(200, rk.angles_linspace(0.0, 2 * np.pi, 40), 300.0)]
 
 
 def _run_threads(fn, n):
@@ -38,10 +42,11 @@ def _run_threads(fn, n):
 def test_threads_on_own_streams_match_serial(rk, cuda):
     gs = _geoms(rk)
     rs = np.random.default_rng(5)
-    xs = [torch.from_numpy(rs.standard_normal((6, 96, 96)).astype(np.float32)).to(cuda) for _ in range(8)]
+    xs = [torch.from_numpy(rs.standard_normal((6, g.image_size, g.image_size)).astype(np.float32)).to(cuda)
+          for g in gs for _ in range(3)]
     ref = []
     for i, x in enumerate(xs):
-        g = gs[i % 2]
+        g = gs[i // 3]
         s = rk.forward(g, x)
         ref.append((s, rk.backprojection(g, s), rk.fbp(g, s)))
     torch.cuda.synchronize()
@@ -50,8 +55,8 @@ def test_threads_on_own_streams_match_serial(rk, cuda):
     def work(i):
         st = torch.cuda.Stream(device=cuda)
         with torch.cuda.stream(st):
-            for _ in range(3):
-                g = gs[i % 2]
+            for _ in range(4):
+                g = gs[i // 3]
                 s = rk.forward(g, xs[i])
                 got[i] = (s, rk.backprojection(g, s), rk.fbp(g, s))
         st.synchronize()
