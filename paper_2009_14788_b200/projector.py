@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 from . import _arrays as A
@@ -48,13 +49,15 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
-            _lib.lib.rk_plan_destroy(h)
+        lib = getattr(_lib, "lib", None) if _lib is not None else None  # None at interpreter shutdown
+        if h is not None and h.value and lib is not None:
+            lib.rk_plan_destroy(h)
             self.handle = None
 
 
-_PLANS: dict = {}
+_PLANS: "OrderedDict" = OrderedDict()  # least recently used first
 _PLANS_LOCK = threading.Lock()
+_MAX_PLANS = 64
 
 
 def get_plan(g: Geometry, opts: ProjectorOptions | None = None, device: int = 0) -> Plan:
@@ -65,9 +68,11 @@ def get_plan(g: Geometry, opts: ProjectorOptions | None = None, device: int = 0)
     with _PLANS_LOCK:
         p = _PLANS.get(key)
         if p is None:
-            if len(_PLANS) > 64:
-                _PLANS.clear()
+            while len(_PLANS) >= _MAX_PLANS:  # evict the least recently used plan (callers keep theirs alive)
+                _PLANS.popitem(last=False)
             p = _PLANS[key] = Plan(g, step, device)
+        else:
+            _PLANS.move_to_end(key)
         return p
 
 

@@ -48,8 +48,9 @@ class _Handle:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
-            _lib.lib.rk_shearlet_destroy(h)
+        lib = getattr(_lib, "lib", None) if _lib is not None else None  # None at interpreter shutdown
+        if h is not None and h.value and lib is not None:
+            lib.rk_shearlet_destroy(h)
             self.h = None
 
 

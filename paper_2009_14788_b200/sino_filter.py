@@ -52,8 +52,9 @@ class _DeviceFilter:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
-            _lib.lib.rk_filter_destroy(h)
+        lib = getattr(_lib, "lib", None) if _lib is not None else None  # None at interpreter shutdown
+        if h is not None and h.value and lib is not None:
+            lib.rk_filter_destroy(h)
             self.handle = None
 
 

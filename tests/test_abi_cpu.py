@@ -170,3 +170,26 @@ def test_host_only_plan_refuses_kernels(rk):
     st = _lib.lib.rk_forward(h, _lib.RK_F32, p, 1, p, None)
     assert st == _lib.RK_ERR_VALIDATION and b"host-only" in _lib.lib.rk_last_error()
     _lib.check(_lib.lib.rk_plan_destroy(h))
+
+
+def test_plan_cache_is_lru(rk):
+    """get_plan keeps the most recently used plans (host-only plans here) and evicts the oldest."""
+    import math
+
+    from paper_2009_14788_b200 import projector as P
+
+    old = P._MAX_PLANS
+    try:
+        P._MAX_PLANS = 3
+        P._PLANS.clear()
+        gs = [rk.make_parallel(16 + i, rk.angles_linspace(0.0, math.pi, 8)) for i in range(4)]
+        a = rk.get_plan(gs[0], None, -1)
+        rk.get_plan(gs[1], None, -1)
+        assert rk.get_plan(gs[0], None, -1) is a  # hit refreshes gs[0]
+        rk.get_plan(gs[2], None, -1)
+        rk.get_plan(gs[3], None, -1)  # evicts gs[1], the least recently used
+        assert [k[0].image_size for k in P._PLANS] == [16, 18, 19]
+        assert rk.get_plan(gs[0], None, -1) is a
+    finally:
+        P._MAX_PLANS = old
+        P._PLANS.clear()
