@@ -611,9 +611,16 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
       const Cell* w = win + q * window;
-      // parallel: the column term is shared by the thread's pixels (one column)
-      float col0 = 0.f;
+      // parallel: the column term is shared by the thread's pixels (one column);
+      // fan (fp32 map): the row terms (a thread's pixels share one row)
+      float col0 = 0.f, nrow = 0.f, drow = 0.f;
       if constexpr (KIND == kBpParallel) col0 = fmaf(float(tx), k.cx, k.base);
+      if constexpr (KIND == kBpFan32) {
+        int pr0, pc0;
+        pixel_of(tid, 0, pr0, pc0);
+        nrow = k.b * float(pr0);
+        drow = fmaf(k.d, float(pr0), k.den00);
+      }
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         int pr, pc;
@@ -623,8 +630,8 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
         if constexpr (KIND == kBpParallel) {
           kf = fmaf(ly, k.cy, col0);
         } else if constexpr (KIND == kBpFan32) {
-          const float num = fmaf(k.b, ly, k.a * lx);             // (qx - qx00) K - u00 (den - den00)
-          const float den = fmaf(k.d, ly, fmaf(k.c, lx, k.den00));  // qy + D_so
+          const float num = fmaf(k.a, lx, nrow);  // (qx - qx00) K - u00 (den - den00)
+          const float den = fmaf(k.c, lx, drow);  // qy + D_so
           kf = fmaf(num, rcp_approx(den), k.base);
         } else {
           const double dlx = double(lx), dly = double(ly);
