@@ -92,7 +92,7 @@ void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, doubl
             int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             int worst = 1;
             for (int u = 0; u < used; ++u)
-              if (first[u]) worst = std::max(worst, ++cnt[int((((ti[u] * pitch + tj[u]) % 8) + 8) % 8)]);
+              if (first[u]) worst = std::max(worst, ++cnt[int((ti[u] * pitch + tj[u]) & 7)]);  // mod 8 (two's complement)
             cost[sw][r] += weight * worst;
           }
         }
