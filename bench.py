@@ -38,7 +38,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-from paper_2009_14788_b200.phantom import shepp_logan as rk_phantom  # noqa: E402  (synthetic input)
+# The product package (and so libradon_b200.so) is imported only inside the
+# "ours" arm: the --impl reference arm must map nothing but oracle/_ref.
 
 GLOBAL_BATCH = 128
 METRIC = "forward+back-projection images/s (512², 512 angles, batch 128) at 1/2/4/8 GPUs"
@@ -152,9 +153,66 @@ def cpu_reference_images_per_s(wl, budget_s=15.0, warmup=1, fixed_batch=None):
     b = fixed_batch or max(1, min(64, int(budget_s / 5.0 / max(t1, 1e-3))))
     times = [run(b) for _ in range(5)]  # 1 warm-up + >= 5 timed runs, median
     med = statistics.median(times)
-    return {"value": b / med, "unit": "images/s", "cores": cores, "kind": kind,
+    return {"value": b / med, "unit": "images/s", "cores": cores, "kind": kind, **cpu_info(orc),
             "sample": f"{b} x {s}^2 image(s), {na} angles, {nd} cells per run; median of 5 runs after 1 warm-up; "
                       f"{'parallel' if k == 'parallel' else 'fan-beam'}; set_num_threads({cores})"}
+
+
+def cpu_info(orc):
+    """Host CPU model (lscpu 'Model name') and which build of the reference ran (oracle/Makefile)."""
+    from oracle import cpu_model
+
+    so = getattr(orc, "path", None)
+    return {"cpu_model": cpu_model(), "march": getattr(orc, "march", "x86-64-v3 (port, -O3)"),
+            "library": os.path.relpath(so, ROOT) if so else "oracle/_port/liboracle.so"}
+
+
+def bench_parity(k, s, na, stop, nd, src, imgs, sino, out):
+    """rel-L2 (tensor.cpp:406-418) of the benched outputs against the reference on the same inputs."""
+    from oracle import Geom, default_oracle, rel_l2
+
+    orc = default_oracle()
+    if hasattr(orc, "set_num_threads"):
+        orc.set_num_threads(os.cpu_count() or 1)
+    g = Geom(k, s, orc.angles_linspace(0.0, stop, na), nd, None, src)
+    ref_sino = orc.forward(g, imgs)
+    ref_bp = orc.backprojection(g, sino)
+    fw = [rel_l2(sino[e], ref_sino[e]) for e in range(len(imgs))]
+    bp = [rel_l2(out[e], ref_bp[e]) for e in range(len(imgs))]
+    return {"max_rel_l2": max(fw + bp), "forward": fw, "backprojection": bp, "tolerance": 1e-5,
+            "elements": "0 (phantom x 1/128), 1 (Rng(1) uniform) of the timed batch; bp checked on the GPU sinogram",
+            "oracle": os.path.relpath(getattr(orc, "path", "oracle/_port/liboracle.so"), ROOT)}
+
+
+def reference_cfg5(args, orc, kind, cores):
+    """--impl reference --workload cfg5: the reference's landweber (solvers.cpp:130-145), 50
+    iterations, one image of the config-5 batch per step (the bounded sample)."""
+    from oracle import Geom
+
+    g = Geom("parallel", 512, orc.angles_linspace(0.0, math.pi, 256))
+    x = orc.shepp_logan(512) * np.float32(1.0 / 256.0)
+    y = orc.forward(g, x)
+    alpha = 0.95 * orc.estimate_alpha(g, 20, 0) if hasattr(orc, "estimate_alpha") else 1e-5
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        orc.landweber(g, y, np.zeros_like(x), alpha, 50)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps / tot
+    line = {
+        "impl": "reference", "metric": "reconstructed images/s (50 Landweber iterations, 512^2, 256 angles, batch 256)",
+        "value": value, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": 0,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "fp32 state, fp64 accumulate", "data": "synthetic: shepp_logan(512) / 256",
+        "config": {"workload": "cfg5: parallel 512x512, linspace(0, pi, 256), 512 cells, global batch 256, "
+                               "50 iterations", "sample_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind, **cpu_info(orc),
+                         "sample": "1 image x 50 Landweber iterations per step"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def run_reference_arm(args):
@@ -173,6 +231,8 @@ def run_reference_arm(args):
     cores = os.cpu_count() or 1
     if kind == "reference":
         orc.set_num_threads(cores)
+    if args.workload == "cfg5":
+        return reference_cfg5(args, orc, kind, cores)
     k, s, na, stop, nd, src, B = WORKLOADS[args.workload]
     g = Geom(k, s, orc.angles_linspace(0.0, stop, na), nd, None, src)
     ph = orc.shepp_logan(s)
@@ -198,7 +258,7 @@ def run_reference_arm(args):
         "data": "synthetic: modified Shepp-Logan phantom (reference shepp_logan)",
         "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
                    "sample_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind, **cpu_info(orc),
                          "sample": f"{per_step} image(s) per step of the {args.workload} workload"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -212,9 +272,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="par512", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="par512", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed outputs")
     ap.add_argument("--no-extras", action="store_true", help="skip the config 3/4/5 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -226,17 +287,38 @@ def main():
 
     import paper_2009_14788_b200 as rk
     from paper_2009_14788_b200 import _lib
+    from paper_2009_14788_b200.phantom import shepp_logan as rk_phantom  # synthetic input
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
+    # RK_BENCH_SHARE_DEVICE=1: every rank on cuda:0 — exercises the multi-rank path (init,
+    # barriers, max-over-ranks, sharding) on a one-GPU box; NCCL rejects two ranks on one
+    # device, so that mode defaults to gloo (RK_BENCH_BACKEND overrides either default).
+    share = os.environ.get("RK_BENCH_SHARE_DEVICE", "0") == "1"
+    gpu = 0 if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     dist = None
+    backend = os.environ.get("RK_BENCH_BACKEND", "gloo" if share else "nccl")
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(v):
+        """Device-timed value -> max over ranks (the contract's multi-GPU time)."""
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if args.workload == "cfg5":
+        return run_cfg5(args, rk, _lib, torch, dist, dev, gpu, world, rank, backend, max_over_ranks)
 
     k, s, na, stop, nd, src, B = WORKLOADS[args.workload]
     ang = rk.angles_linspace(0.0, stop, na)
@@ -258,7 +340,7 @@ def main():
     sino = torch.empty(nb, na, nd, device=dev)
     out = torch.empty(nb, s, s, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    plan = rk.get_plan(g, None, local)
+    plan = rk.get_plan(g, None, gpu)
     info = plan.info()
     stream = torch.cuda.current_stream(dev)
     sp = ctypes_void(stream.cuda_stream)
@@ -274,11 +356,11 @@ def main():
     torch.cuda.synchronize(dev)
 
     smem_peak = ctypes_double()
-    _lib.check(_lib.lib.rk_probe_smem_bandwidth(local, smem_peak))
+    _lib.check(_lib.lib.rk_probe_smem_bandwidth(gpu, smem_peak))
     stats = _lib.RkKernelStats()
     _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     clocks.start()
     time.sleep(0.3)
     _lib.check(_lib.lib.rk_profiling_enable(1))
@@ -298,11 +380,7 @@ def main():
     _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    if dist is not None:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
     value = B / (ms_per_step * 1e-3)
 
@@ -346,6 +424,13 @@ def main():
                                     "ms": bp_ms, "gbs": bp_bytes / (bp_ms * 1e-3) / 1e9,
                                     "gsamples_per_s": info["backproject_samples"] * nb / (bp_ms * 1e-3) / 1e9}}}
 
+    # ---- parity of the timed step's own outputs (checker only, outside every timed region):
+    # rel-L2 of elements 0-1 of this rank's shard against the reference (oracle/_ref) on the
+    # benched geometry: forward on the input images, backprojection on the GPU's sinogram.
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = bench_parity(k, s, na, stop, nd, src, imgs[:2], sino[:2].cpu().numpy(), out[:2].cpu().numpy())
+
     # ---- end to end through the reference-shaped host-buffer API
     e2e = None
     if not args.no_e2e:
@@ -366,11 +451,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_step()
-        el = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([el], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_over_ranks(time.perf_counter() - t0)
         bi = 4 * nb * (s * s + na * nd)
         e2e = {"value": B * args.steps / el, "unit": "images/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi,
                "ms_per_step": 1e3 * el / args.steps,
@@ -394,9 +475,89 @@ def main():
             "data": "synthetic: modified Shepp-Logan phantom x (e+1)/128 for even e, Rng(e) uniform for odd e",
             "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
                        "global_batch": B, "per_gpu_batch": nb, "parallelism": f"batch-shard x{world}, no collective",
+                       "dist_backend": backend if world > 1 else None, "shared_device": share,
                        "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kern,
+            "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kern,
             "clocks": clk, "other_configs": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_cfg5(args, rk, _lib, torch, dist, dev, gpu, world, rank, backend, max_over_ranks):
+    """--workload cfg5 (BASELINE configs[4]): 50 Landweber iterations
+    (solvers.cpp:130-145, alpha = 0.95 estimate_alpha(op, 20, seed 0)) on parallel 512^2,
+    linspace(0, pi, 256), 512 cells, global batch 256 sharded over the ranks with no collective;
+    50 CGNE iterations (solvers.cpp:147-166) measured beside it.  A step = one solve of this
+    rank's shard; device time by CUDA events, max over ranks."""
+    from paper_2009_14788_b200.phantom import shepp_logan
+    from paper_2009_14788_b200.sharding import shard_range
+
+    B, iters = 256, 50
+    g = rk.make_parallel(512, rk.angles_linspace(0.0, math.pi, 256))
+    op = rk.projector_operator(g)
+    lo, hi = shard_range(B, world, rank)
+    nb = hi - lo
+    ph = shepp_logan(512)
+    x = torch.from_numpy(np.stack([ph * np.float32((e + 1) / float(B)) for e in range(lo, hi)])).to(dev)
+    y = rk.forward(g, x)
+    z = torch.zeros_like(x)
+    alpha = 0.95 * rk.estimate_alpha(op, 20, 0)  # deterministic: every rank derives the same step
+    st = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn, steps):
+        tot = 0.0
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            torch.cuda.synchronize(dev)
+            tot += a.elapsed_time(b)
+        return tot
+
+    lw = lambda: rk.landweber(op, y, z, alpha, iters)  # noqa: E731
+    cg = lambda: rk.cgne(op, z, y, iters)  # noqa: E731
+    for _ in range(args.warmup):
+        lw()
+    cg()
+    torch.cuda.synchronize(dev)
+    stats = _lib.RkKernelStats()
+    _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
+    clocks = ClockSampler(gpu)
+    clocks.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms_lw = max_over_ranks(timed(lw, args.steps))
+    _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
+    launches = int(sum(stats.launches[i] for i in range(len(_lib.KERNEL_KINDS))))
+    ms_cg = max_over_ranks(timed(cg, max(1, args.steps // 2)))
+    clk = clocks.stop()
+    if dist is not None:
+        dist.barrier()
+    per_lw = ms_lw / args.steps
+    per_cg = ms_cg / max(1, args.steps // 2)
+    if rank == 0:
+        line = {
+            "metric": "reconstructed images/s (50 Landweber iterations, 512^2, 256 angles, batch 256)",
+            "value": B / (per_lw * 1e-3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_lw, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic: shepp_logan(512) x (e+1)/256",
+            "config": {"workload": "cfg5: parallel 512x512, linspace(0, pi, 256), 512 cells, global batch 256, "
+                                   "50 iterations", "global_batch": B, "per_gpu_batch": nb,
+                       "parallelism": f"batch-shard x{world}, no collective",
+                       "dist_backend": backend if world > 1 else None, "alpha": alpha,
+                       "alpha_note": "0.95 * estimate_alpha(op, 20, seed 0), computed once outside the timed region",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
+            "cgne": {"value": B / (per_cg * 1e-3), "unit": "images/s", "ms_per_step": per_cg,
+                     "steps": max(1, args.steps // 2)},
+            "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -407,6 +568,8 @@ def main():
 def measure_extras(rk, _lib, dev):
     """Device-timed numbers for the other BASELINE configs (N=1 only; 1 warm-up + 3 runs each)."""
     import torch
+
+    from paper_2009_14788_b200.phantom import shepp_logan as rk_phantom  # synthetic input
 
     out = {}
     st = torch.cuda.current_stream(dev)

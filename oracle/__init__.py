@@ -32,7 +32,40 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-REF_SO = os.path.join(_HERE, "_ref", "libradonkit_ref.so")
+REF_SO = os.path.join(_HERE, "_ref", "libradonkit_ref.so")        # -march=x86-64-v3
+REF_SO_V4 = os.path.join(_HERE, "_ref", "libradonkit_ref_v4.so")  # -march=x86-64-v4 (AVX-512)
+_V4_FLAGS = ("avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl")
+
+
+def _cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu 'Model name'), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def best_ref_so() -> str:
+    """The highest-ISA build of the reference this host can run (oracle/Makefile: the
+    travelling stand-in for -march=native)."""
+    if os.path.exists(REF_SO_V4) and all(f in _cpu_flags() for f in _V4_FLAGS):
+        return REF_SO_V4
+    return REF_SO
 PORT_SO = os.path.join(_HERE, "_port", "liboracle.so")
 
 FILTERS = ["ram-lak", "shepp-logan", "cosine", "hamming", "hann"]  # sino_filter.cpp:14-33
@@ -98,7 +131,10 @@ def _ptr(a: np.ndarray):
 class RefOracle:
     """ctypes face of the reference compiled in place (see module doc)."""
 
-    def __init__(self, path: str = REF_SO):
+    def __init__(self, path: str | None = None):
+        path = path or best_ref_so()
+        self.path = path
+        self.march = "x86-64-v4" if path == REF_SO_V4 else "x86-64-v3"
         if not os.path.exists(path):
             raise FileNotFoundError(f"reference oracle not built: {path} (run `make -C oracle ref`)")
         self.lib = ctypes.CDLL(path)

@@ -15,6 +15,25 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Device-restoring scope of one C-ABI call (see rk::set_device).  Nested entry
+// points (rk_admm -> rk_admm_create ...) share the outermost scope.
+thread_local int g_scope_depth = 0;
+thread_local int g_saved_device = -1;
+
+struct DeviceScope {
+  DeviceScope() {
+    if (g_scope_depth++ == 0) g_saved_device = -1;
+  }
+  ~DeviceScope() {
+    if (--g_scope_depth == 0 && g_saved_device >= 0) {
+      int cur = -1;
+      if (cudaGetDevice(&cur) == cudaSuccess && cur != g_saved_device) cudaSetDevice(g_saved_device);
+      cudaGetLastError();  // a failed restore must not surface as the next launch's error
+      g_saved_device = -1;
+    }
+  }
+};
+
 // NVTX range per C-ABI call (header-only NVTX v3: a no-op unless a profiler
 // such as Nsight Systems injects itself), named after the entry point.
 struct NvtxRange {
@@ -25,6 +44,7 @@ struct NvtxRange {
 template <class F>
 int guarded_named(const char* name, F&& f) {
   NvtxRange range(name);
+  DeviceScope device_scope;
   try {
     f();
     return RK_OK;
@@ -56,7 +76,7 @@ struct ScratchLease {
   cudaStream_t st;
   std::lock_guard<std::mutex> lock;
   ScratchLease(rk::Plan& plan, cudaStream_t stream) : p(plan), st(stream), lock(plan.mu) {
-    RK_CUDA(cudaSetDevice(p.device));
+    rk::set_device(p.device);
     RK_CUDA(cudaStreamWaitEvent(st, p.scratch_free, 0));
   }
   ~ScratchLease() { cudaEventRecord(p.scratch_free, st); }
@@ -134,15 +154,17 @@ bool is_pinned(const void* p) {
   return attr.type == cudaMemoryTypeHost;
 }
 
+// Runs under the owner's lock; `wait_first` (the plan's scratch event) is
+// synchronised first, so device-pointer calls still using scratch finish.
 template <class Body>
-void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_item, const void* h_in, void* h_out,
-                       Body body) {
-  std::lock_guard<std::mutex> lock(p.mu);
-  RK_CUDA(cudaSetDevice(p.device));
-  for (auto& s : p.copy_streams)
+void run_host_pipeline(rk::HostPipeline& pipe, int device, std::mutex& mu, int64_t batch, size_t in_item,
+                       size_t out_item, const void* h_in, void* h_out, cudaEvent_t wait_first, Body body) {
+  std::lock_guard<std::mutex> lock(mu);
+  rk::set_device(device);
+  for (auto& s : pipe.streams)
     if (!s) RK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   // host calls are synchronous: wait for any device-pointer call still using scratch
-  RK_CUDA(cudaEventSynchronize(p.scratch_free));
+  if (wait_first) RK_CUDA(cudaEventSynchronize(wait_first));
   // ~8 chunks, each a whole number of packed groups and >= 4 MB of input
   int64_t chunk = std::max<int64_t>(rk::kPack, (batch + 7) / 8);
   chunk = (chunk + rk::kPack - 1) / rk::kPack * rk::kPack;
@@ -150,9 +172,10 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
   min_items = (min_items + rk::kPack - 1) / rk::kPack * rk::kPack;
   chunk = std::min(batch, std::max(chunk, min_items));
   const bool pinned_in = is_pinned(h_in), pinned_out = is_pinned(h_out);
-  for (int i = 0; i < rk::Plan::kPipeSlots; ++i) {
-    p.pipe_in[i].reserve(size_t(chunk) * in_item);
-    p.pipe_out[i].reserve(size_t(chunk) * out_item);
+  constexpr int kSlots = rk::HostPipeline::kSlots;
+  for (int i = 0; i < kSlots; ++i) {
+    pipe.in[i].reserve(size_t(chunk) * in_item);
+    pipe.out[i].reserve(size_t(chunk) * out_item);
   }
   // chunk sizes: ramp up from one packed group and back down at the end, so
   // the copy-in before the first kernel and the copy-out after the last one
@@ -171,19 +194,45 @@ void run_host_pipeline(rk::Plan& p, int64_t batch, size_t in_item, size_t out_it
   int slot = 0;
   int64_t b0 = 0;
   for (const int64_t nb : sizes) {
-    cudaStream_t st = p.copy_streams[slot];
+    cudaStream_t st = pipe.streams[slot];
     const char* src = static_cast<const char*>(h_in) + size_t(b0) * in_item;
     char* dst = static_cast<char*>(h_out) + size_t(b0) * out_item;
-    RK_CUDA(cudaMemcpyAsync(p.pipe_in[slot].ptr, src, size_t(nb) * in_item, cudaMemcpyHostToDevice, st));
-    body(p.pipe_in[slot].ptr, nb, p.pipe_out[slot].ptr, slot, st);
-    RK_CUDA(cudaMemcpyAsync(dst, p.pipe_out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
+    RK_CUDA(cudaMemcpyAsync(pipe.in[slot].ptr, src, size_t(nb) * in_item, cudaMemcpyHostToDevice, st));
+    body(pipe.in[slot].ptr, nb, pipe.out[slot].ptr, slot, st);
+    RK_CUDA(cudaMemcpyAsync(dst, pipe.out[slot].ptr, size_t(nb) * out_item, cudaMemcpyDeviceToHost, st));
     if (!pinned_in || !pinned_out) RK_CUDA(cudaStreamSynchronize(st));
     b0 += nb;
-    slot = (slot + 1) % rk::Plan::kPipeSlots;
+    slot = (slot + 1) % kSlots;
   }
-  for (auto s : p.copy_streams) RK_CUDA(cudaStreamSynchronize(s));
+  for (auto s : pipe.streams) RK_CUDA(cudaStreamSynchronize(s));
 }
 
+}  // namespace
+
+void rk::set_device(int device) {
+  if (g_scope_depth > 0 && g_saved_device < 0) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess)
+      g_saved_device = cur;
+    else
+      cudaGetLastError();
+  }
+  RK_CUDA(cudaSetDevice(device));
+}
+
+namespace {
+// Waits for a plan's own device work (its scratch-reuse event and copy
+// streams) before teardown, instead of draining the whole device; errors are
+// deliberately ignored here and cleared so they cannot surface later.
+void quiesce_plan(rk::Plan& p) {
+  if (p.device < 0) return;
+  if (cudaSetDevice(p.device) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (p.scratch_free) cudaEventSynchronize(p.scratch_free);
+  p.pipe.synchronize();
+}
 }  // namespace
 
 extern "C" {
@@ -233,9 +282,12 @@ int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan) {
 int rk_plan_destroy(rk_plan* plan) {
   return guarded_named(__func__, [&] {
     if (!plan) return;
-    cudaSetDevice(plan->p.device);
-    cudaDeviceSynchronize();
-    delete plan;
+    {
+      std::lock_guard<std::mutex> lock(plan->p.mu);  // no call is enqueueing on it
+      quiesce_plan(plan->p);
+    }
+    delete plan;  // frees on the plan's device (current after quiesce_plan)
+    cudaGetLastError();
   });
 }
 
@@ -306,9 +358,13 @@ int rk_filter_create(int kind, int64_t det_count, int device, rk_filter** filter
 int rk_filter_destroy(rk_filter* filter) {
   return guarded_named(__func__, [&] {
     if (!filter) return;
-    cudaSetDevice(filter->f.device);
-    cudaDeviceSynchronize();
+    if (filter->f.device >= 0) {
+      // the filter's tables may still be read by kernels enqueued on any stream
+      if (cudaSetDevice(filter->f.device) == cudaSuccess) cudaDeviceSynchronize();
+      cudaGetLastError();
+    }
     delete filter;
+    cudaGetLastError();
   });
 }
 
@@ -332,7 +388,7 @@ int rk_filter_sinogram(rk_filter* filter, int dtype, const void* d_in, int64_t b
     require(d_in != nullptr && d_out != nullptr, "sinogram pointer is null");
     rk::Filter& f = filter->f;
     std::lock_guard<std::mutex> lock(f.mu);
-    RK_CUDA(cudaSetDevice(f.device));
+    rk::set_device(f.device);
     rk::launch_filter(f, dtype, d_in, batch, n_angles, d_out, nullptr, as_stream(stream));
   });
 }
@@ -363,9 +419,10 @@ int rk_forward_host(rk_plan* plan, int dtype, const void* h_image, int64_t batch
     require(h_image != nullptr && h_sino != nullptr, "image / sinogram pointer is null");
     rk::Plan& p = plan->p;
     const size_t es = rk::dtype_size(dtype);
-    run_host_pipeline(p, batch, size_t(p.s * p.s) * es, size_t(p.na * p.nd) * es, h_image, h_sino,
+    run_host_pipeline(p.pipe, p.device, p.mu, batch, size_t(p.s * p.s) * es, size_t(p.na * p.nd) * es, h_image,
+                      h_sino, p.scratch_free,
                       [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
-                        forward_into(p, dtype, din, nb, dout, p.pipe_pk[slot], p.pipe_pkt[slot], st);
+                        forward_into(p, dtype, din, nb, dout, p.pipe.pk[slot], p.pipe.pkt[slot], st);
                       });
   });
 }
@@ -378,9 +435,10 @@ int rk_backproject_host(rk_plan* plan, int dtype, const void* h_sino, int64_t ba
     require(h_image != nullptr && h_sino != nullptr, "image / sinogram pointer is null");
     rk::Plan& p = plan->p;
     const size_t es = rk::dtype_size(dtype);
-    run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
+    run_host_pipeline(p.pipe, p.device, p.mu, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino,
+                      h_image, p.scratch_free,
                       [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
-                        backproject_into(p, dtype, din, nb, dout, p.pipe_pk[slot], st);
+                        backproject_into(p, dtype, din, nb, dout, p.pipe.pk[slot], st);
                       });
   });
 }
@@ -393,15 +451,11 @@ int rk_filter_sinogram_host(rk_filter* filter, int dtype, const void* h_in, int6
     require(batch >= 1 && n_angles >= 1, "sinogram must have batch >= 1 and n_angles >= 1");
     require(h_in != nullptr && h_out != nullptr, "sinogram pointer is null");
     rk::Filter& f = filter->f;
-    std::lock_guard<std::mutex> lock(f.mu);
-    RK_CUDA(cudaSetDevice(f.device));
-    const size_t bytes = size_t(batch * n_angles * f.det_count) * rk::dtype_size(dtype);
-    rk::DeviceBuffer din, dout;
-    din.reserve(bytes);
-    dout.reserve(bytes);
-    RK_CUDA(cudaMemcpy(din.ptr, h_in, bytes, cudaMemcpyHostToDevice));
-    rk::launch_filter(f, dtype, din.ptr, batch, n_angles, dout.ptr, nullptr, nullptr);
-    RK_CUDA(cudaMemcpy(h_out, dout.ptr, bytes, cudaMemcpyDeviceToHost));
+    const size_t item = size_t(n_angles * f.det_count) * rk::dtype_size(dtype);  // one sinogram
+    run_host_pipeline(f.pipe, f.device, f.mu, batch, item, item, h_in, h_out, nullptr,
+                      [&](const void* din, int64_t nb, void* dout, int, cudaStream_t st) {
+                        rk::launch_filter(f, dtype, din, nb, n_angles, dout, nullptr, st);
+                      });
   });
 }
 
@@ -415,10 +469,12 @@ int rk_fbp_host(rk_plan* plan, rk_filter* filter, int dtype, const void* h_sino,
     rk::Plan& p = plan->p;
     require(filter->f.det_count == p.nd, "sinogram det_count " + std::to_string(p.nd) +
                                              " does not match filter " + std::to_string(filter->f.det_count));
+    require(filter->f.device == p.device, "filter and plan live on different devices");
     const size_t es = rk::dtype_size(dtype);
-    run_host_pipeline(p, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino, h_image,
+    run_host_pipeline(p.pipe, p.device, p.mu, batch, size_t(p.na * p.nd) * es, size_t(p.s * p.s) * es, h_sino,
+                      h_image, p.scratch_free,
                       [&](const void* din, int64_t nb, void* dout, int slot, cudaStream_t st) {
-                        fbp_into(p, filter->f, dtype, din, nb, dout, p.pipe_pk[slot], st);
+                        fbp_into(p, filter->f, dtype, din, nb, dout, p.pipe.pk[slot], st);
                       });
   });
 }
@@ -518,10 +574,11 @@ int rk_shearlet_destroy(rk_shearlet* plan) {
   return guarded_named(__func__, [&] {
     if (!plan) return;
     if (plan->s.device >= 0) {
-      cudaSetDevice(plan->s.device);
-      cudaDeviceSynchronize();
+      if (cudaSetDevice(plan->s.device) == cudaSuccess) cudaDeviceSynchronize();
+      cudaGetLastError();
     }
     delete plan;
+    cudaGetLastError();
   });
 }
 
@@ -544,7 +601,7 @@ int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
     std::lock_guard<std::mutex> lock(plan->s.mu);
-    RK_CUDA(cudaSetDevice(plan->s.device));
+    rk::set_device(plan->s.device);
     rk::shearlet_forward(plan->s, dtype, d_image, batch, d_coeff, as_stream(stream));
   });
 }
@@ -558,7 +615,7 @@ int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int6
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
     std::lock_guard<std::mutex> lock(plan->s.mu);
-    RK_CUDA(cudaSetDevice(plan->s.device));
+    rk::set_device(plan->s.device);
     rk::shearlet_backward(plan->s, dtype, d_coeff, batch, d_image, as_stream(stream));
   });
 }
@@ -647,7 +704,7 @@ int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* s
     require(d_dst != nullptr, "destination pointer is null");
     check_dtype(dtype);
     rk::Admm& a = admm->a;
-    RK_CUDA(cudaSetDevice(a.plan->device));
+    rk::set_device(a.plan->device);
     RK_CUDA(cudaStreamWaitEvent(as_stream(stream), a.plan->scratch_free, 0));
     rk::admm_read(a, which, dtype, d_dst, as_stream(stream));
   });
@@ -656,9 +713,10 @@ int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* s
 int rk_admm_destroy(rk_admm_state* admm) {
   return guarded_named(__func__, [&] {
     if (!admm) return;
-    cudaSetDevice(admm->a.plan->device);
-    cudaDeviceSynchronize();
+    if (cudaSetDevice(admm->a.plan->device) == cudaSuccess) cudaDeviceSynchronize();
+    cudaGetLastError();
     delete admm;
+    cudaGetLastError();
   });
 }
 

@@ -35,8 +35,17 @@ void DeviceBuffer::reserve(size_t n) {
 
 Plan::~Plan() {
   if (scratch_free) cudaEventDestroy(scratch_free);
-  for (auto& s : copy_streams)
+}
+
+HostPipeline::~HostPipeline() {
+  for (auto& s : streams)
     if (s) cudaStreamDestroy(s);
+}
+
+void HostPipeline::synchronize() {
+  for (auto s : streams)
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
 }
 
 size_t dtype_size(int dtype) {
@@ -164,7 +173,7 @@ void ensure_forward_schedule(Plan& p) {
     std::vector<RayD> rays = compute_rays(p, angle_trig(p), nullptr);
     std::vector<float4> rg, ra;
     build_forward_plan(p, rays, rg, ra);
-    RK_CUDA(cudaSetDevice(p.device));
+    rk::set_device(p.device);
     p.ray_geom.reserve(rg.size() * sizeof(float4));
     p.ray_aux.reserve(ra.size() * sizeof(float4));
     RK_CUDA(cudaMemcpy(p.ray_geom.ptr, rg.data(), rg.size() * sizeof(float4), cudaMemcpyHostToDevice));
@@ -281,7 +290,7 @@ void build_plan(Plan& p) {
 
   // ----- upload (device < 0: host-only plan, used for inspection on machines without a GPU)
   if (p.device < 0) return;
-  RK_CUDA(cudaSetDevice(p.device));
+  rk::set_device(p.device);
   p.trig.reserve(trig.size() * sizeof(double2));
   RK_CUDA(cudaMemcpy(p.trig.ptr, trig.data(), trig.size() * sizeof(double2), cudaMemcpyHostToDevice));
   p.bp_tile_window.reserve(tile_window.size() * sizeof(int));
@@ -392,7 +401,7 @@ void build_filter(Filter& f, int kind, int64_t det_count) {
     tw[size_t(k)] = make_float2(float(std::cos(ang)), float(-std::sin(ang)));
   }
   if (f.device < 0) return;  // host-only filter (response inspection without a GPU)
-  RK_CUDA(cudaSetDevice(f.device));
+  rk::set_device(f.device);
   f.d_response.reserve(f.response_f.size() * sizeof(float));
   f.d_twiddle.reserve(tw.size() * sizeof(float2));
   RK_CUDA(cudaMemcpy(f.d_response.ptr, f.response_f.data(), f.response_f.size() * sizeof(float),

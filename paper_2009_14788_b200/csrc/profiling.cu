@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kProbeThreads) smem_probe_kernel(float* out, i
 }  // namespace
 
 double probe_smem_bandwidth(int device) {
-  RK_CUDA(cudaSetDevice(device));
+  rk::set_device(device);
   int sms = 0;
   RK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   float* out = nullptr;

@@ -34,6 +34,12 @@ struct CudaError : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define RK_CUDA(call) ::rk::cuda_check((call), #call)
 
+// Makes `device` current for the rest of the enclosing C-ABI call.  The first
+// switch inside a call remembers the caller's device, and the call restores it
+// on return (capi.cpp DeviceScope), so a call on a cuda:1 plan never moves the
+// calling thread's current device — torch shares that context state.
+void set_device(int device);
+
 // ----------------------------------------------------------------- device buffers
 struct DeviceBuffer {
   void* ptr = nullptr;
@@ -93,6 +99,23 @@ struct ForwardSchedule {
   std::vector<int2> warps;  // per CTA x 8 warps {angle (-1: idle), first detector cell}
 };
 
+// ----------------------------------------------------------------- host pipelines
+// Scratch of the reference-shaped host-buffer calls (rk_*_host): chunks of the
+// batch stream through kSlots non-blocking streams, each with its own device
+// buffers, so one chunk's copy-in, another's kernels and a third's copy-out
+// overlap.  Grown on demand, kept for the owner's lifetime (no per-call
+// allocation once warm).
+struct HostPipeline {
+  static constexpr int kSlots = 3;
+  cudaStream_t streams[kSlots] = {nullptr, nullptr, nullptr};
+  DeviceBuffer in[kSlots], out[kSlots], pk[kSlots], pkt[kSlots];
+  HostPipeline() = default;
+  HostPipeline(const HostPipeline&) = delete;
+  HostPipeline& operator=(const HostPipeline&) = delete;
+  ~HostPipeline();
+  void synchronize();  // waits for every slot's stream (errors ignored and cleared)
+};
+
 // ----------------------------------------------------------------- plan
 struct Plan;
 void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<float4>& ray_geom,
@@ -132,10 +155,7 @@ struct Plan {
   std::mutex mu;
   DeviceBuffer packed_image, packed_image_t, packed_sino;
   cudaEvent_t scratch_free = nullptr;
-  // host-buffer (*_host) pipelines: two streams, each with its own buffers
-  static constexpr int kPipeSlots = 3;  // chunks in flight: copy-in, kernels, copy-out overlap
-  cudaStream_t copy_streams[kPipeSlots] = {nullptr, nullptr, nullptr};
-  DeviceBuffer pipe_in[kPipeSlots], pipe_out[kPipeSlots], pipe_pk[kPipeSlots], pipe_pkt[kPipeSlots];
+  HostPipeline pipe;  // host-buffer (*_host) calls
   // solver scratch
   DeviceBuffer solver_a, solver_b, solver_c, solver_d, solver_scalars;
 
@@ -151,6 +171,7 @@ struct Filter {
   std::vector<float> response_f;  // same, float (sino_filter.cpp:89)
   DeviceBuffer d_response;        // float, padded/2+1
   DeviceBuffer d_twiddle;         // float2, padded/2 (forward twiddles)
+  HostPipeline pipe;              // rk_filter_sinogram_host
   std::mutex mu;
 };
 

@@ -635,7 +635,7 @@ void upload_shearlet(Shearlet& sp) {
   if (sp.device < 0) return;
   std::vector<float2> m2, tw;
   build_tables<float>(sp, m2, tw);
-  RK_CUDA(cudaSetDevice(sp.device));
+  rk::set_device(sp.device);
   sp.d_mult2.reserve(m2.size() * sizeof(float2));
   sp.d_twiddle.reserve(tw.size() * sizeof(float2));
   RK_CUDA(cudaMemcpy(sp.d_mult2.ptr, m2.data(), m2.size() * sizeof(float2), cudaMemcpyHostToDevice));

@@ -65,15 +65,19 @@ def get_plan(g: Geometry, opts: ProjectorOptions | None = None, device: int = 0)
     if not (step > 0.0):  # projector.cpp:31-33
         raise ValidationError("projector step must be positive")
     key = (g, step, int(device))
+    evicted = []
     with _PLANS_LOCK:
         p = _PLANS.get(key)
         if p is None:
             while len(_PLANS) >= _MAX_PLANS:  # evict the least recently used plan (callers keep theirs alive)
-                _PLANS.popitem(last=False)
+                evicted.append(_PLANS.popitem(last=False)[1])
             p = _PLANS[key] = Plan(g, step, device)
         else:
             _PLANS.move_to_end(key)
-        return p
+    # the evicted plans are released here, outside the lock: rk_plan_destroy waits for the plan's
+    # own in-flight work, which must not stall other threads' get_plan calls
+    del evicted
+    return p
 
 
 def _check_geometry(g):

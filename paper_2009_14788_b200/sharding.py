@@ -22,8 +22,11 @@ def shard_range(batch: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def gather_batch(local, global_batch: int, dst: int = 0, group=None):
-    """Concatenate every rank's shard on rank `dst` (torch.distributed; NCCL for
-    CUDA tensors, gloo for CPU).  Returns the full batch on `dst`, None elsewhere."""
+    """Concatenate every rank's shard on rank `dst` (torch.distributed: NCCL
+    all-gather for CUDA tensors; gloo gathers through host memory, so CUDA
+    shards under gloo — e.g. several ranks sharing one GPU, which NCCL
+    rejects — are staged on the CPU).  Returns the full batch on `dst`, on the
+    shard's device, None elsewhere."""
     import torch
     import torch.distributed as dist
 
@@ -31,13 +34,16 @@ def gather_batch(local, global_batch: int, dst: int = 0, group=None):
     rank = dist.get_rank(group)
     per = -(-int(global_batch) // world)
     shape = tuple(local.shape[1:])
-    padded = torch.zeros((per, *shape), dtype=local.dtype, device=local.device)
-    padded[: local.shape[0]] = local
-    parts = [torch.empty_like(padded) for _ in range(world)] if rank == dst else None
-    if dist.get_backend(group) == "nccl":
+    nccl = dist.get_backend(group) == "nccl"
+    home = local.device
+    work = home if nccl else torch.device("cpu")
+    padded = torch.zeros((per, *shape), dtype=local.dtype, device=work)
+    padded[: local.shape[0]] = local.to(work)
+    if nccl:
         parts = [torch.empty_like(padded) for _ in range(world)]
         dist.all_gather(parts, padded, group=group)
     else:
+        parts = [torch.empty_like(padded) for _ in range(world)] if rank == dst else None
         dist.gather(padded, parts, dst=dst, group=group)
     if rank != dst:
         return None
@@ -45,7 +51,7 @@ def gather_batch(local, global_batch: int, dst: int = 0, group=None):
     for r in range(world):
         lo, hi = shard_range(global_batch, world, r)
         out.append(parts[r][: hi - lo])
-    return torch.cat(out, 0)
+    return torch.cat(out, 0).to(home)
 
 
 def shard_numpy(x: np.ndarray, world: int, rank: int) -> np.ndarray:

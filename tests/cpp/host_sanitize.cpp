@@ -12,6 +12,7 @@
 
 namespace rk {
 void upload_shearlet(Shearlet&) {}  // device-side table upload (shearlet.cu): not part of this host test
+void set_device(int device) { RK_CUDA(cudaSetDevice(device)); }  // capi.cpp's scope-restoring switch; host-only plans never call it
 }  // namespace rk
 
 static void plan(int kind, int64_t s, const std::vector<double>& ang, int64_t nd, double sp, double src, double dd,

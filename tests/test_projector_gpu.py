@@ -317,3 +317,29 @@ def test_small_batch_wide_backprojection_equals_batched_bitwise(rk, oracle, cuda
     small = rk.backprojection(g, dev(y[:4], cuda))
     assert torch.equal(small, full[:4])
     assert rel_l2(host(small), oracle.backprojection(ogeom(g), y[:4])) <= TOL32
+
+
+def test_host_only_plan_teardown_leaves_no_cuda_error(rk, oracle, cuda):
+    """A host-only plan / filter (device -1) destroyed in a process that then launches kernels:
+    teardown must neither fail nor leave a sticky CUDA error for the next launch."""
+    import gc
+
+    import ctypes
+
+    from paper_2009_14788_b200 import _lib
+    from paper_2009_14788_b200.projector import Plan
+
+    g = par(rk, 32, 20)
+    hp = Plan(g, 1.0, -1)
+    assert hp.info()["device"] == -1
+    del hp
+    gc.collect()
+    fh = ctypes.c_void_p()
+    _lib.check(_lib.lib.rk_filter_create(0, 32, -1, ctypes.byref(fh)))
+    _lib.check(_lib.lib.rk_filter_destroy(fh))
+    x = dev(batched_phantom(oracle, 32, 2), cuda)
+    before = torch.cuda.current_device()
+    sino = rk.forward(g, x)
+    torch.cuda.synchronize()
+    assert torch.cuda.current_device() == before
+    assert rel_l2(host(sino), oracle.forward(ogeom(g), host(x))) <= TOL32

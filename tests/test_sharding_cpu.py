@@ -31,6 +31,48 @@ def _free_port():
     return p
 
 
+def _projector_worker(rank, world, port, B, q):
+    """Each rank runs the reference projector (the CPU oracle, the checker) on its shard only;
+    the gathered result must equal the single-process batch bit for bit (acceptance.cpp:340-389)."""
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import Geom, PortOracle, batched_phantom
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = PortOracle()
+    g = Geom("parallel", 24, orc.angles_linspace(0.0, np.pi, 18))
+    full = batched_phantom(orc, 24, B)
+    lo, hi = shard_range(B, world, rank)
+    local = torch.from_numpy(orc.forward(g, full[lo:hi]))
+    out = gather_batch(local, B)
+    if rank == 0:
+        q.put(bool(np.array_equal(out.numpy(), orc.forward(g, full))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [5, 8])
+def test_gloo_world2_sharded_projector(B):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_projector_worker, args=(r, 2, port, B, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5) is True
+
+
 def _worker(rank, world, port, B, q):
     import torch
     import torch.distributed as dist
