@@ -301,7 +301,9 @@ def main():
     dev = torch.device("cuda", gpu)
     dist = None
     backend = os.environ.get("RK_BENCH_BACKEND", "gloo" if share else "nccl")
-    if world > 1:
+    # RK_BENCH_FORCE_DIST=1: initialise the process group even at world size 1, so a one-GPU box
+    # runs the real NCCL init / barrier / max-reduce lines (NCCL rejects two ranks on one device)
+    if world > 1 or os.environ.get("RK_BENCH_FORCE_DIST", "0") == "1":
         import torch.distributed as dist
 
         if backend == "nccl":
@@ -475,7 +477,7 @@ def main():
             "data": "synthetic: modified Shepp-Logan phantom x (e+1)/128 for even e, Rng(e) uniform for odd e",
             "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
                        "global_batch": B, "per_gpu_batch": nb, "parallelism": f"batch-shard x{world}, no collective",
-                       "dist_backend": backend if world > 1 else None, "shared_device": share,
+                       "dist_backend": backend if dist is not None else None, "shared_device": share,
                        "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
             "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kern,
             "clocks": clk, "other_configs": extras,
@@ -552,7 +554,7 @@ def run_cfg5(args, rk, _lib, torch, dist, dev, gpu, world, rank, backend, max_ov
             "config": {"workload": "cfg5: parallel 512x512, linspace(0, pi, 256), 512 cells, global batch 256, "
                                    "50 iterations", "global_batch": B, "per_gpu_batch": nb,
                        "parallelism": f"batch-shard x{world}, no collective",
-                       "dist_backend": backend if world > 1 else None, "alpha": alpha,
+                       "dist_backend": backend if dist is not None else None, "alpha": alpha,
                        "alpha_note": "0.95 * estimate_alpha(op, 20, seed 0), computed once outside the timed region",
                        "l2": "flushed (256 MiB write) between timed steps, outside the timed events"},
             "cgne": {"value": B / (per_cg * 1e-3), "unit": "images/s", "ms_per_step": per_cg,
