@@ -460,6 +460,9 @@ def main():
                "path": "rk_forward_host + rk_backproject_host (pinned host buffers, 3-stream chunked copy/compute "
                        "pipeline, synchronous like the reference's Tensor-in/Tensor-out calls)"}
 
+    if e2e is not None and rank == 0:
+        e2e["first_call_ms"] = first_call_latency(rk, _lib, g, gpu, imgs[:1])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_images_per_s(args.workload)
@@ -486,6 +489,45 @@ def main():
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def first_call_latency(rk, _lib, g, gpu, img1):
+    """One-shot latency of the reference-shaped call (projector.cpp:228-236: a stateless forward):
+    a new plan + the first rk_forward_host of one image (host buffers, copies included), with the
+    forward schedule planned from scratch ("cold": empty plan cache), read from the on-disk plan
+    cache ("warm_cache": a new process projecting a geometry seen before), and a second call on the
+    same plan ("steady")."""
+    import tempfile
+
+    from paper_2009_14788_b200.projector import Plan
+
+    na, nd = g.n_angles, g.det_count
+    out = np.empty((1, na, nd), np.float32)
+    saved = os.environ.get("RK_PLAN_CACHE")
+    res = {}
+    try:
+        os.environ["RK_PLAN_CACHE"] = tempfile.mkdtemp(prefix="rk_bench_cache_")
+        for key in ("cold", "warm_cache"):
+            t0 = time.perf_counter()
+            p = Plan(g, 1.0, gpu)
+            _lib.check(_lib.lib.rk_forward_host(p.handle, _lib.RK_F32, ctypes_void(img1.ctypes.data), 1,
+                                                ctypes_void(out.ctypes.data)))
+            res[key] = 1e3 * (time.perf_counter() - t0)
+            if key == "warm_cache":
+                assert p.info()["schedule_from_cache"]
+                t0 = time.perf_counter()
+                _lib.check(_lib.lib.rk_forward_host(p.handle, _lib.RK_F32, ctypes_void(img1.ctypes.data), 1,
+                                                    ctypes_void(out.ctypes.data)))
+                res["steady"] = 1e3 * (time.perf_counter() - t0)
+            del p
+    finally:
+        if saved is None:
+            os.environ.pop("RK_PLAN_CACHE", None)
+        else:
+            os.environ["RK_PLAN_CACHE"] = saved
+    res["what"] = ("new plan + first rk_forward_host of 1 image (pageable host buffers): schedule planned (cold), "
+                   "read from the plan cache (warm_cache); steady = the next call on the same plan")
+    return res
 
 
 def run_cfg5(args, rk, _lib, torch, dist, dev, gpu, world, rank, backend, max_over_ranks):

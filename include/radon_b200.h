@@ -100,8 +100,12 @@ typedef struct rk_plan_info {
   int64_t forward_samples;      /* exact sum over rays of max(1, ceil(len/step))       */
   int64_t backproject_samples;  /* s * s * n_angles                                    */
   int32_t device;               /* CUDA device the plan lives on                       */
-  int32_t reserved;
+  int32_t flags;                /* RK_PLAN_* bits below                                */
 } rk_plan_info;
+
+/* rk_plan_info.flags */
+#define RK_PLAN_SCHEDULED 1       /* the forward schedule exists (first forward / rk_plan_prepare done) */
+#define RK_PLAN_SCHEDULE_CACHED 2 /* ... and came from the on-disk plan cache ($RK_PLAN_CACHE)          */
 
 /* ------------------------------------------------------------- misc */
 const char* rk_last_error(void);
@@ -121,6 +125,11 @@ int rk_angles_linspace(double start, double stop, int64_t n, double* out);
 int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan);
 int rk_plan_destroy(rk_plan* plan);
 int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info);
+/* Builds (or loads from the plan cache) the forward schedule now instead of on
+ * the first rk_forward — the planning the reference's stateless forward
+ * (projector.cpp:228-236) never pays; `hash` (optional) receives a 64-bit
+ * FNV-1a digest of the schedule tables (equal digests = identical launches). */
+int rk_plan_prepare(rk_plan* plan, uint64_t* hash);
 
 /* ------------------------------------------------------------- projector */
 /* image: batch x s x s (dtype) -> sino: batch x n_angles x det_count (dtype). */

@@ -41,7 +41,7 @@ class RkPlanInfo(ctypes.Structure):
         ("forward_samples", ctypes.c_int64),
         ("backproject_samples", ctypes.c_int64),
         ("device", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),  # RK_PLAN_SCHEDULED | RK_PLAN_SCHEDULE_CACHED
     ]
 
 
@@ -56,6 +56,7 @@ SIGNATURES = {
     "rk_plan_create": (_i, [_P(RkGeometry), _i, _P(_vp)]),
     "rk_plan_destroy": (_i, [_vp]),
     "rk_plan_info_get": (_i, [_vp, _P(RkPlanInfo)]),
+    "rk_plan_prepare": (_i, [_vp, _P(_u64)]),
     "rk_forward": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
     "rk_backproject": (_i, [_vp, _i, _vp, _i64, _vp, _vp]),
     "rk_filter_kind_from_name": (_i, [ctypes.c_char_p, _P(_i)]),

@@ -300,7 +300,20 @@ int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info) {
     info->forward_samples = p.forward_samples;
     info->backproject_samples = p.s * p.s * p.na;
     info->device = p.device;
-    info->reserved = 0;
+    const bool built = !p.fwd.cta.empty();
+    info->flags = (built ? RK_PLAN_SCHEDULED : 0) | (built && p.fwd.from_cache ? RK_PLAN_SCHEDULE_CACHED : 0);
+  });
+}
+
+int rk_plan_prepare(rk_plan* plan, uint64_t* hash) {
+  return guarded_named(__func__, [&] {
+    check_plan(plan);
+    rk::Plan& p = plan->p;
+    {
+      std::lock_guard<std::mutex> lock(p.mu);
+      rk::ensure_forward_schedule(p);  // host-only plans scheduled at creation
+    }
+    if (hash) *hash = rk::schedule_hash(p.fwd);
   });
 }
 

@@ -51,21 +51,51 @@ inline Pt to_pixel(double x, double y, double half) { return {x + half + 0.5, ha
 // right column first — the kernel issues each lane's four taps in that order)
 // and row-pitch residue mod 8, the sum over quarter warps and taps of the
 // number of distinct 16-byte cells that share a slot (1 = conflict free).
+//
+// The slot of cell (i, j) under residue r is (j + r i) mod 8 (pitch 64 + r).
+// For the eight residues at once, a cell contributes one count to slot
+// (j + r i) & 7 of residue r: eight 4-bit counters (one 32-bit word) per
+// residue, so a cell's contribution is an 8-word vector that depends only on
+// (i mod 8, j mod 8) — a table lookup and one vector add per distinct cell.
+// The worst slot of each residue is then found with one threshold test per
+// count level (counts are at most 8, so nibble + 8 - t carries into the
+// nibble's top bit exactly when nibble >= t).
+typedef uint32_t V8 __attribute__((vector_size(32)));
+
+struct SlotTable {
+  V8 inc[64];  // [(i & 7) * 8 + (j & 7)]
+  SlotTable() {
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j)
+        for (int r = 0; r < 8; ++r) inc[i * 8 + j][r] = 1u << (4 * ((j + r * i) & 7));
+  }
+};
+const SlotTable kSlots;
+
+inline V8 worst_slot(const V8& cnt) {
+  V8 worst = {1, 1, 1, 1, 1, 1, 1, 1};
+  for (uint32_t t = 2; t <= 8; ++t)
+    worst -= ((cnt + (0x11111111u * (8u - t))) & 0x88888888u) != 0u;  // -1 where some nibble >= t
+  return worst;
+}
+
+// AVX2 where the host has it (the vector code is 256-bit wide), baseline x86-64 otherwise.
+__attribute__((target_clones("avx2", "default")))
 void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, double cost[3][8]) {
-  for (int sw = 0; sw < 3; ++sw)
-    for (int r = 0; r < 8; ++r) cost[sw][r] = 0.0;
+  V8 acc[3];  // per swap, per residue (integer sums; exact)
+  for (auto& a : acc) a = V8{0, 0, 0, 0, 0, 0, 0, 0};
   const int nw = int(lanes_at_step.size()) / 32;
   for (int w = 0; w < nw; ++w) {
     for (int q = 0; q < 32; q += 8) {
-      int64_t bi[8], bj[8];
+      int32_t bi[8], bj[8];  // padded-image cells: far inside 32 bits
       int lane_of[8];
       int used = 0;
       for (int l = 0; l < 8; ++l) {
         const Pt& pt = lanes_at_step[size_t(w * 32 + q + l)];
         if (std::isnan(pt.px)) continue;
         const double cx = transposed ? pt.py : pt.px, cy = transposed ? pt.px : pt.py;
-        bj[used] = int64_t(std::floor(cx));
-        bi[used] = int64_t(std::floor(cy));
+        bj[used] = int32_t(std::floor(cx));
+        bi[used] = int32_t(std::floor(cy));
         lane_of[used] = q + l;
         ++used;
       }
@@ -76,28 +106,25 @@ void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, doubl
       // the tap matters.  So 5 of the 12 (swap, tap) patterns are evaluated.
       for (int sw = 0; sw < 3; ++sw)
         for (int tap = 0; tap < 4; ++tap) {
-          const int weight = sw == 0 ? (tap == 0 ? 4 : 0) : sw == 1 ? ((tap & 1) ? 0 : 2) : ((tap & 2) ? 0 : 2);
+          const uint32_t weight = sw == 0 ? (tap == 0 ? 4 : 0) : sw == 1 ? ((tap & 1) ? 0 : 2) : ((tap & 2) ? 0 : 2);
           if (!weight) continue;
-          int64_t ti[8], tj[8];
-          bool first[8];
+          uint64_t key[8];
+          V8 cnt = {0, 0, 0, 0, 0, 0, 0, 0};
           for (int u = 0; u < used; ++u) {
             const bool odd = (lane_of[u] & 1) != 0;
-            ti[u] = bi[u] + ((sw == 1 && odd) ? 1 - (tap >> 1) : (tap >> 1));
-            tj[u] = bj[u] + ((sw == 2 && odd) ? 1 - (tap & 1) : (tap & 1));
-            first[u] = true;
-            for (int v = 0; v < u && first[u]; ++v) first[u] = !(ti[v] == ti[u] && tj[v] == tj[u]);
+            const int32_t ti = bi[u] + ((sw == 1 && odd) ? 1 - (tap >> 1) : (tap >> 1));
+            const int32_t tj = bj[u] + ((sw == 2 && odd) ? 1 - (tap & 1) : (tap & 1));
+            key[u] = (uint64_t(uint32_t(ti)) << 32) | uint32_t(tj);
+            bool first = true;
+            for (int v = 0; v < u; ++v) first &= key[v] != key[u];
+            if (first) cnt += kSlots.inc[((ti & 7) << 3) | (tj & 7)];  // mod 8 (two's complement)
           }
-          for (int r = 0; r < 8; ++r) {
-            const int64_t pitch = 64 + r;
-            int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            int worst = 1;
-            for (int u = 0; u < used; ++u)
-              if (first[u]) worst = std::max(worst, ++cnt[int((ti[u] * pitch + tj[u]) & 7)]);  // mod 8 (two's complement)
-            cost[sw][r] += weight * worst;
-          }
+          acc[sw] += weight * worst_slot(cnt);
         }
     }
   }
+  for (int sw = 0; sw < 3; ++sw)
+    for (int r = 0; r < 8; ++r) cost[sw][r] = double(acc[sw][r]);
 }
 
 // Conflict-free reference for conflict_cost: one wavefront per quarter warp
@@ -210,6 +237,33 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   }
 
   ForwardSchedule& F = p.fwd;
+  // Checks and diagnostics of the final schedule (planned or from the cache).
+  auto finish = [&]() {
+    if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
+    if (std::getenv("RK_DEBUG_PLAN")) {
+      int64_t ntr = 0;
+      for (const int4& c : F.cta) ntr += c.z & 1;
+      const uint64_t hsh = schedule_hash(F);  // A/B: same schedule?
+      std::fprintf(stderr, "[rk] forward schedule: hash %016llx%s\n", (unsigned long long)hsh,
+                   F.from_cache ? " (from the plan cache)" : "");
+      std::fprintf(stderr, "[rk] forward schedule: lane mappings (angles per quarter warp 1/2/4/8) %d/%d/%d/%d CTAs, "
+                   "simulated wavefronts %.3fx conflict-free\n", F.mapping_count[0], F.mapping_count[1],
+                   F.mapping_count[2], F.mapping_count[3], F.sim_cost / std::max(F.sim_ideal, 1.0));
+      std::fprintf(stderr,
+                   "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
+                   "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
+                   F.shape_aa, F.shape_db, F.cta.size(), (long long)ntr, F.boxes.size(),
+                   double(F.boxes.size()) / double(std::max<size_t>(F.cta.size(), 1)), (long long)F.max_box,
+                   double(F.max_box) * 16.0 / 1024.0, double(F.staged_texels) / 1e6);
+    }
+  };
+  const std::vector<unsigned char> cache_key = schedule_cache_key(p);
+  const std::string cache_path = schedule_cache_path(cache_key);
+  if (load_schedule(cache_path, cache_key, P2, F)) {
+    F.from_cache = true;
+    finish();
+    return;
+  }
   std::vector<int> order(static_cast<size_t>(na));
   for (int64_t a = 0; a < na; ++a) order[size_t(a)] = int(a);
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
@@ -567,20 +621,8 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       F.cta = std::move(cta2);
       F.warps = std::move(warps2);
     }
-    if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
-    if (std::getenv("RK_DEBUG_PLAN")) {
-      int64_t ntr = 0;
-      for (const int4& c : F.cta) ntr += c.z & 1;
-      std::fprintf(stderr, "[rk] forward schedule: lane mappings (angles per quarter warp 1/2/4/8) %d/%d/%d/%d CTAs, "
-                   "simulated wavefronts %.3fx conflict-free\n", F.mapping_count[0], F.mapping_count[1],
-                   F.mapping_count[2], F.mapping_count[3], F.sim_cost / std::max(F.sim_ideal, 1.0));
-      std::fprintf(stderr,
-                   "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
-                   "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
-                   sh.aa, sh.db, F.cta.size(), (long long)ntr, F.boxes.size(),
-                   double(F.boxes.size()) / double(F.cta.size()), (long long)F.max_box,
-                   double(F.max_box) * 16.0 / 1024.0, double(F.staged_texels) / 1e6);
-    }
+    store_schedule(cache_path, cache_key, F);
+    finish();
     return;
   }
   throw ValidationError("forward schedule: a staged image box exceeds shared memory even for the shortest chunk");

@@ -91,6 +91,7 @@ struct ForwardSchedule {
   int64_t staged_texels = 0;       // per image group, all CTAs and chunks
   bool any_transposed = false;
   double sim_cost = 0.0, sim_ideal = 0.0;  // planner's simulated shared-memory wavefronts (chosen, conflict-free)
+  bool from_cache = false;                 // loaded from the on-disk schedule cache (plan_cache.cpp)
   int mapping_count[4] = {0, 0, 0, 0};      // CTAs per lane mapping (log2 angles per quarter warp)
   // per chunk {row0 | col0 << 16, rows | cols << 16, pitch, t_end (float bits; inf = last)},
   // in staged-image coordinates, CTA after CTA
@@ -120,6 +121,14 @@ struct HostPipeline {
 struct Plan;
 void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<float4>& ray_geom,
                         std::vector<float4>& ray_aux);
+
+// On-disk schedule cache (plan_cache.cpp): key = planner version + geometry
+// + planner knobs; path "" when the cache is disabled.
+std::vector<unsigned char> schedule_cache_key(const Plan& p);
+std::string schedule_cache_path(const std::vector<unsigned char>& key);
+bool load_schedule(const std::string& path, const std::vector<unsigned char>& key, int64_t padded, ForwardSchedule& F);
+uint64_t schedule_hash(const ForwardSchedule& F);  // FNV-1a over boxes, CTA records, warps
+void store_schedule(const std::string& path, const std::vector<unsigned char>& key, const ForwardSchedule& F);
 
 // Builds and uploads the plan's forward schedule once (plan.cpp); every
 // forward launch path calls it first.

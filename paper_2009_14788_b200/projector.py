@@ -45,7 +45,16 @@ class Plan:
         _lib.check(_lib.lib.rk_plan_info_get(self.handle, ctypes.byref(inf)))
         return {"forward_samples": int(inf.forward_samples), "backproject_samples": int(inf.backproject_samples),
                 "device": int(inf.device), "det_count": int(inf.geometry.det_count),
-                "det_spacing": float(inf.geometry.det_spacing)}
+                "det_spacing": float(inf.geometry.det_spacing),
+                "scheduled": bool(inf.flags & 1), "schedule_from_cache": bool(inf.flags & 2)}
+
+    def prepare(self) -> int:
+        """Plan the forward schedule now (else the first forward does): loads it from the on-disk
+        plan cache ($RK_PLAN_CACHE, default ~/.cache/radon_b200) or plans and stores it; returns
+        the schedule's 64-bit digest (equal digests = identical launches)."""
+        h = ctypes.c_uint64()
+        _lib.check(_lib.lib.rk_plan_prepare(self.handle, ctypes.byref(h)))
+        return int(h.value)
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -9,6 +9,14 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# Forward schedules go to a per-session plan cache (plan_cache.cpp), so the
+# suite neither reads nor fills the user's ~/.cache/radon_b200.
+if "RK_PLAN_CACHE" not in os.environ:
+    import tempfile
+
+    os.environ["RK_PLAN_CACHE"] = tempfile.mkdtemp(prefix="rk_plan_cache_")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: full-size configuration checks")

@@ -22,7 +22,7 @@ def test_host_planners_asan_ubsan(tmp_path):
     cmd = ["g++", "-std=c++20", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
            "-fno-omit-frame-pointer", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-I", os.path.join(CUDA, "include"), os.path.join(ROOT, "tests", "cpp", "host_sanitize.cpp")]
-    cmd += [os.path.join(CSRC, f) for f in ("plan.cpp", "fwd_plan.cpp", "shearlet_plan.cpp")]
+    cmd += [os.path.join(CSRC, f) for f in ("plan.cpp", "fwd_plan.cpp", "plan_cache.cpp", "shearlet_plan.cpp")]
     cmd += ["-L", os.path.join(CUDA, "lib64"), "-lcudart", "-lpthread", "-o", exe]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     env = dict(os.environ, RK_VERIFY_PLAN="1", ASAN_OPTIONS="detect_leaks=1:abort_on_error=0",
