@@ -167,7 +167,7 @@ def cpu_info(orc):
             "library": os.path.relpath(so, ROOT) if so else "oracle/_port/liboracle.so"}
 
 
-def bench_parity(k, s, na, stop, nd, src, imgs, sino, out):
+def bench_parity(k, s, na, stop, nd, src, imgs, sino, out, tol=1e-5):
     """rel-L2 (tensor.cpp:406-418) of the benched outputs against the reference on the same inputs."""
     from oracle import Geom, default_oracle, rel_l2
 
@@ -179,7 +179,7 @@ def bench_parity(k, s, na, stop, nd, src, imgs, sino, out):
     ref_bp = orc.backprojection(g, sino)
     fw = [rel_l2(sino[e], ref_sino[e]) for e in range(len(imgs))]
     bp = [rel_l2(out[e], ref_bp[e]) for e in range(len(imgs))]
-    return {"max_rel_l2": max(fw + bp), "forward": fw, "backprojection": bp, "tolerance": 1e-5,
+    return {"max_rel_l2": max(fw + bp), "forward": fw, "backprojection": bp, "tolerance": tol,
             "elements": "0 (phantom x 1/128), 1 (Rng(1) uniform) of the timed batch; bp checked on the GPU sinogram",
             "oracle": os.path.relpath(getattr(orc, "path", "oracle/_port/liboracle.so"), ROOT)}
 
@@ -275,6 +275,8 @@ def main():
     ap.add_argument("--workload", default="par512", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp16"],
+                    help="storage dtype of images and sinograms (fp32 compute either way; projector.cpp:207-224)")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed outputs")
     ap.add_argument("--no-extras", action="store_true", help="skip the config 3/4/5 side measurements")
     args = ap.parse_args()
@@ -338,9 +340,15 @@ def main():
             imgs[i] = ph * np.float32((e + 1) / 128.0)
         else:
             imgs[i] = rk.Rng(e).uniform_tensor((s, s))
+    fp16 = args.dtype == "fp16"
+    tdt = torch.float16 if fp16 else torch.float32
+    rkdt = _lib.RK_F16 if fp16 else _lib.RK_F32
+    esz = 2 if fp16 else 4
+    if fp16:  # x 1/8: the backprojection of a 512-angle sinogram stays inside the half range (65504)
+        imgs = (imgs * np.float32(0.125)).astype(np.float16)
     x = torch.from_numpy(imgs).to(dev)
-    sino = torch.empty(nb, na, nd, device=dev)
-    out = torch.empty(nb, s, s, device=dev)
+    sino = torch.empty(nb, na, nd, device=dev, dtype=tdt)
+    out = torch.empty(nb, s, s, device=dev, dtype=tdt)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     plan = rk.get_plan(g, None, gpu)
     info = plan.info()
@@ -348,9 +356,9 @@ def main():
     sp = ctypes_void(stream.cuda_stream)
 
     def step():
-        _lib.check(_lib.lib.rk_forward(plan.handle, _lib.RK_F32, ctypes_void(x.data_ptr()), nb,
+        _lib.check(_lib.lib.rk_forward(plan.handle, rkdt, ctypes_void(x.data_ptr()), nb,
                                        ctypes_void(sino.data_ptr()), sp))
-        _lib.check(_lib.lib.rk_backproject(plan.handle, _lib.RK_F32, ctypes_void(sino.data_ptr()), nb,
+        _lib.check(_lib.lib.rk_backproject(plan.handle, rkdt, ctypes_void(sino.data_ptr()), nb,
                                            ctypes_void(out.data_ptr()), sp))
 
     for _ in range(args.warmup):
@@ -393,8 +401,10 @@ def main():
             for i in range(len(kinds)) if stats.launches[i]}
     # roofline of the dominant kernel: algorithmic L1TEX/SMEM bytes per launch
     # (16 B per forward sample = 4 fp32 taps; 8 B per backprojection sample = 2 taps)
-    fwd_bytes = 16.0 * info["forward_samples"] * nb
-    bp_bytes = 8.0 * info["backproject_samples"] * nb
+    # fp16 storage: 4 taps x 2 B forward, 2 taps x 2 B backprojection
+    fwd_bps, bp_bps = (8, 4) if fp16 else (16, 8)
+    fwd_bytes = float(fwd_bps) * info["forward_samples"] * nb
+    bp_bytes = float(bp_bps) * info["backproject_samples"] * nb
     fwd_ms = kern.get("forward", {}).get("ms_per_launch") or float("nan")
     bp_ms = kern.get("backproject", {}).get("ms_per_launch") or float("nan")
     dom, dbytes, dms = ("forward", fwd_bytes, fwd_ms) if fwd_ms >= bp_ms else ("backproject", bp_bytes, bp_ms)
@@ -419,10 +429,10 @@ def main():
                 "hbm_check": hbm_check(traffic, dms),
                 "algorithmic_bytes_per_launch": dbytes,
                 "per_kernel": {
-                    "forward": {"samples_per_launch": info["forward_samples"] * nb, "bytes_per_sample": 16,
+                    "forward": {"samples_per_launch": info["forward_samples"] * nb, "bytes_per_sample": fwd_bps,
                                 "ms": fwd_ms, "gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9,
                                 "gsamples_per_s": info["forward_samples"] * nb / (fwd_ms * 1e-3) / 1e9},
-                    "backproject": {"samples_per_launch": info["backproject_samples"] * nb, "bytes_per_sample": 8,
+                    "backproject": {"samples_per_launch": info["backproject_samples"] * nb, "bytes_per_sample": bp_bps,
                                     "ms": bp_ms, "gbs": bp_bytes / (bp_ms * 1e-3) / 1e9,
                                     "gsamples_per_s": info["backproject_samples"] * nb / (bp_ms * 1e-3) / 1e9}}}
 
@@ -431,19 +441,20 @@ def main():
     # benched geometry: forward on the input images, backprojection on the GPU's sinogram.
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = bench_parity(k, s, na, stop, nd, src, imgs[:2], sino[:2].cpu().numpy(), out[:2].cpu().numpy())
+        parity = bench_parity(k, s, na, stop, nd, src, imgs[:2], sino[:2].cpu().numpy(), out[:2].cpu().numpy(),
+                              1e-3 if fp16 else 1e-5)
 
     # ---- end to end through the reference-shaped host-buffer API
     e2e = None
     if not args.no_e2e:
         h_img = torch.from_numpy(imgs).pin_memory()
-        h_sino = torch.empty(nb, na, nd).pin_memory()
-        h_out = torch.empty(nb, s, s).pin_memory()
+        h_sino = torch.empty(nb, na, nd, dtype=tdt).pin_memory()
+        h_out = torch.empty(nb, s, s, dtype=tdt).pin_memory()
 
         def e2e_step():
-            _lib.check(_lib.lib.rk_forward_host(plan.handle, _lib.RK_F32, ctypes_void(h_img.data_ptr()), nb,
+            _lib.check(_lib.lib.rk_forward_host(plan.handle, rkdt, ctypes_void(h_img.data_ptr()), nb,
                                                 ctypes_void(h_sino.data_ptr())))
-            _lib.check(_lib.lib.rk_backproject_host(plan.handle, _lib.RK_F32, ctypes_void(h_sino.data_ptr()), nb,
+            _lib.check(_lib.lib.rk_backproject_host(plan.handle, rkdt, ctypes_void(h_sino.data_ptr()), nb,
                                                     ctypes_void(h_out.data_ptr())))
 
         for _ in range(2):
@@ -454,14 +465,14 @@ def main():
         for _ in range(args.steps):
             e2e_step()
         el = max_over_ranks(time.perf_counter() - t0)
-        bi = 4 * nb * (s * s + na * nd)
+        bi = esz * nb * (s * s + na * nd)
         e2e = {"value": B * args.steps / el, "unit": "images/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi,
                "ms_per_step": 1e3 * el / args.steps,
                "path": "rk_forward_host + rk_backproject_host (pinned host buffers, 3-stream chunked copy/compute "
                        "pipeline, synchronous like the reference's Tensor-in/Tensor-out calls)"}
 
     if e2e is not None and rank == 0:
-        e2e["first_call_ms"] = first_call_latency(rk, _lib, g, gpu, imgs[:1])
+        e2e["first_call_ms"] = first_call_latency(rk, _lib, g, gpu, np.ascontiguousarray(imgs[:1], np.float32))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -476,8 +487,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic: modified Shepp-Logan phantom x (e+1)/128 for even e, Rng(e) uniform for odd e",
+            "vs_baseline": None, "dtype": "fp16 storage, fp32 compute" if fp16 else "fp32",
+            "data": "synthetic: modified Shepp-Logan phantom x (e+1)/128 for even e, Rng(e) uniform for odd e"
+                    + (", x 1/8 in fp16 storage" if fp16 else ""),
             "config": {"workload": f"{args.workload}: {k} {s}x{s}, {na} angles, {nd} detectors, global batch {B}",
                        "global_batch": B, "per_gpu_batch": nb, "parallelism": f"batch-shard x{world}, no collective",
                        "dist_backend": backend if dist is not None else None, "shared_device": share,
