@@ -90,6 +90,10 @@ __global__ void pack_sino_kernel(const T* __restrict__ src, int64_t batch, int64
 __device__ __forceinline__ unsigned h2_bits(__half lo, __half hi) {
   return unsigned(__half_as_ushort(lo)) | (unsigned(__half_as_ushort(hi)) << 16);
 }
+// word w of a half8 texel -> images 2w, 2w+1 as floats (exact)
+__device__ __forceinline__ float2 h8_pair(unsigned w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
 __device__ __forceinline__ unsigned h8_word(const uint4& u, int i) {
   return i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w;
 }
@@ -205,24 +209,6 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
   return *reinterpret_cast<float2*>(&rd);
 }
-// fp16 storage: word w of a half8 texel (images 2w, 2w+1) widened to an f32
-// pair held as one 64-bit register pair, so FFMA2 consumes the two
-// conversions directly (HADD2.F32 x2, no register moves); the conversion is
-// exact, so each lane is still rounded exactly as the scalar fmaf chain.
-__device__ __forceinline__ unsigned long long h2_to_f2(unsigned w) {
-  unsigned long long r;
-  asm("{\n.reg .b16 lo, hi;\n.reg .f32 a, b;\nmov.b32 {lo, hi}, %1;\ncvt.f32.f16 a, lo;\ncvt.f32.f16 b, hi;\n"
-      "mov.b64 %0, {a, b};\n}" : "=l"(r) : "r"(w));
-  return r;
-}
-// acc (f32 pair bits) <- a * b + acc, lane by lane as fmaf (FFMA2, scalar a)
-__device__ __forceinline__ unsigned long long ffma2_bits(float a, unsigned long long b, unsigned long long acc) {
-  float2 aa = make_float2(a, a);
-  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&aa), rd;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(b), "l"(acc));
-  return rd;
-}
-__device__ __forceinline__ float2 f2_of(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
 __device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
 
@@ -308,9 +294,9 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   }
   __syncthreads();
   float2 a01 = make_float2(0.f, 0.f), a23 = a01;  // images 0-1, 2-3 (LANE: a01.x)
-  unsigned long long a8[H8 ? kPackH8 / 2 : 1];     // H8: image pairs (f32 pair bits)
+  float2 a8[H8 ? kPackH8 / 2 : 1];                 // H8: image pairs
 #pragma unroll
-  for (int q = 0; q < (H8 ? kPackH8 / 2 : 1); ++q) a8[q] = 0ull;
+  for (int q = 0; q < (H8 ? kPackH8 / 2 : 1); ++q) a8[q] = make_float2(0.f, 0.f);
   int m = 0;
   // LANE: lane 0 of the box's texels by 4-byte cp.async (warp w takes rows w,
   // w + 8, ...) into two alternating scalar boxes, the next chunk's copies in
@@ -389,11 +375,15 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
         const uint4* q8 = reinterpret_cast<const uint4*>(box_s) + (i * pitch + j + dA);
         const uint4 u1 = q8[0], u2 = q8[dX], u3 = q8[dY], u4 = q8[dY + dX];
 #pragma unroll
-        for (int wd = 0; wd < 4; ++wd)
-          a8[wd] = ffma2_bits(w1, h2_to_f2(h8_word(u1, wd)),
-                              ffma2_bits(w2, h2_to_f2(h8_word(u2, wd)),
-                                         ffma2_bits(w3, h2_to_f2(h8_word(u3, wd)),
-                                                    ffma2_bits(w4, h2_to_f2(h8_word(u4, wd)), a8[wd]))));
+        for (int wd = 0; wd < 4; ++wd) {
+          const float2 f1 = h8_pair(h8_word(u1, wd)), f2 = h8_pair(h8_word(u2, wd));
+          const float2 f3 = h8_pair(h8_word(u3, wd)), f4 = h8_pair(h8_word(u4, wd));
+          // scalar FMAs: FFMA2 on converted pairs (no register moves) measured equal for the forward
+          // and 11 % slower for the backprojection (r2 A/B, tools/ab_bench.sh): the conversions and
+          // FMAs share the FP32 pipe, which FFMA2 occupies for two slots
+          a8[wd].x = fmaf(w1, f1.x, fmaf(w2, f2.x, fmaf(w3, f3.x, fmaf(w4, f4.x, a8[wd].x))));
+          a8[wd].y = fmaf(w1, f1.y, fmaf(w2, f2.y, fmaf(w3, f3.y, fmaf(w4, f4.y, a8[wd].y))));
+        }
       } else {
       const float4* q = box_s + (i * pitch + j + dA);
       const float4 v1 = q[0], v2 = q[dX], v3 = q[dY], v4 = q[dY + dX];
@@ -409,7 +399,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
 #pragma unroll
     for (int q = 0; q < kPackH8; ++q) {
       const int64_t b = g * kPackH8 + q;
-      if (b < batch) sino[b * n_rays8 + r] = from_f32<TOut>((q & 1 ? f2_of(a8[q >> 1]).y : f2_of(a8[q >> 1]).x) * h);
+      if (b < batch) sino[b * n_rays8 + r] = from_f32<TOut>((q & 1 ? a8[q >> 1].y : a8[q >> 1].x) * h);
     }
     return;
   }
@@ -545,11 +535,11 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
   float4 acc[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-  unsigned long long acc8[H8 ? RPT : 1][H8 ? kPackH8 / 2 : 1];  // H8: image pairs (f32 pair bits)
+  float acc8[H8 ? RPT : 1][H8 ? kPackH8 : 1];
 #pragma unroll
   for (int r = 0; r < (H8 ? RPT : 1); ++r)
 #pragma unroll
-    for (int q = 0; q < (H8 ? kPackH8 / 2 : 1); ++q) acc8[r][q] = 0ull;
+    for (int q = 0; q < (H8 ? kPackH8 : 1); ++q) acc8[r][q] = 0.f;
 
   for (int a0 = 0; a0 < na; a0 += chunk) {
     const int nac = min(chunk, na - a0);
@@ -664,8 +654,11 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
           const float4 s0f = w[c0], s1f = w[c0 + 1];
           const uint4 s0 = *reinterpret_cast<const uint4*>(&s0f), s1 = *reinterpret_cast<const uint4*>(&s1f);
 #pragma unroll
-          for (int wd = 0; wd < 4; ++wd)
-            acc8[r][wd] = ffma2_bits(wt, h2_to_f2(h8_word(s1, wd)), ffma2_bits(wl, h2_to_f2(h8_word(s0, wd)), acc8[r][wd]));
+          for (int wd = 0; wd < 4; ++wd) {
+            const float2 f0 = h8_pair(h8_word(s0, wd)), f1 = h8_pair(h8_word(s1, wd));
+            acc8[r][2 * wd] = fmaf(wt, f1.x, fmaf(wl, f0.x, acc8[r][2 * wd]));
+            acc8[r][2 * wd + 1] = fmaf(wt, f1.y, fmaf(wl, f0.y, acc8[r][2 * wd + 1]));
+          }
         } else {
           const float4 s0 = w[c0], s1 = w[c0 + 1];
           const float2 lo = ffma2(wt, lo2(s1), ffma2(wl, lo2(s0), lo2(acc[r])));
@@ -688,7 +681,7 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
 #pragma unroll
       for (int q = 0; q < kPackH8; ++q) {
         const int64_t b = g * kPackH8 + q;
-        if (b < batch) out[(b * s + i) * int64_t(s) + j] = from_f32<TOut>(q & 1 ? f2_of(acc8[r][q >> 1]).y : f2_of(acc8[r][q >> 1]).x);
+        if (b < batch) out[(b * s + i) * int64_t(s) + j] = from_f32<TOut>(acc8[r][q]);
       }
       continue;
     }
