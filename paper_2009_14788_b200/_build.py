@@ -57,6 +57,8 @@ def build_oracles(verbose: bool = False) -> None:
     subprocess.run([make, "-s", "-C", odir, "port"], check=True)
     if os.path.isdir("/root/reference/proj/core/src"):
         subprocess.run([make, "-s", "-C", odir, "ref"], check=True)
+        # the reference's own program over the B200 projector
+        subprocess.run([make, "-s", "-j8", "-C", os.path.join(ROOT, "integration")], check=True)
 
 
 if __name__ == "__main__":
