@@ -10,6 +10,8 @@
 // decimation-in-frequency (natural in, bit-reversed out), the response is
 // applied in bit-reversed order, and the inverse is decimation-in-time with
 // conjugate twiddles (bit-reversed in, natural out): no permutation pass.
+// The row load, the response multiply and the crop/scale/store are fused into
+// the first forward, last forward and last inverse passes (filter_kernel).
 #include <cuda_fp16.h>
 
 #include <type_traits>
@@ -41,9 +43,72 @@ __device__ __forceinline__ double st_cast<double>(float v) { return double(v); }
 
 constexpr int kFilterThreads = 256;
 
+// One fused radix-2^R pass over the two complex sequences (fft_smem.cuh's
+// fft_pass with the same butterflies, twiddles and order, so the transform is
+// bit-identical to it), with the element I/O supplied by the caller:
+//   load(seq, i, m) -> float2    (m: the element's index within the group)
+//   store(seq, i, m, float2)
+// so the first forward pass can read the rows straight from global memory,
+// the last forward pass can apply the response before its store, and the
+// last inverse pass can crop, scale and write the output from registers.
+// ZERO_TOP: inputs i >= n/2 are known zero (the zero-padded half of the row):
+// the group's upper elements are not loaded and the first butterfly layer
+// (partner bit R-1 of a DIF pass at the widest stride) reduces to u, u W.
+template <int R, bool DIF, bool CONJ, bool ZERO_TOP, class Load, class Store>
+__device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, Load load, Store store) {
+  const int gl = logn - R;
+  for (int t = threadIdx.x; t < (2 << gl); t += blockDim.x) {
+    const int seq = t >> gl, g = t & ((1 << gl) - 1);
+    const int lo = g & ((1 << lh) - 1), hi = g >> lh;
+    const int i0 = lo + (hi << (lh + R));
+    float2 x[1 << R];
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m)
+      x[m] = (ZERO_TOP && m >= (1 << (R - 1))) ? make_float2(0.f, 0.f) : load(seq, i0 + (m << lh), m);
+#pragma unroll
+    for (int l = 0; l < R; ++l) {
+      const int bit = DIF ? R - 1 - l : l;
+#pragma unroll
+      for (int m = 0; m < (1 << R); ++m) {
+        if (m & (1 << bit)) continue;
+        const int q = m | (1 << bit);
+        const int k = lo + ((m & ((1 << bit) - 1)) << lh);
+        const float2 w = tw[k << (logn - lh - 1 - bit)];
+        const float2 u = x[m];
+        if (DIF) {
+          if (ZERO_TOP && l == 0) {  // v = 0: u + v = u, (u - v) W = u W
+            x[q] = fft_cmul(u, w);
+          } else {
+            const float2 v = x[q];
+            x[m] = make_float2(u.x + v.x, u.y + v.y);
+            x[q] = fft_cmul(make_float2(u.x - v.x, u.y - v.y), w);
+          }
+        } else {
+          const float2 v = CONJ ? fft_cmul_conj(x[q], w) : fft_cmul(x[q], w);
+          x[m] = make_float2(u.x + v.x, u.y + v.y);
+          x[q] = make_float2(u.x - v.x, u.y - v.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < (1 << R); ++m) store(seq, i0 + (m << lh), m, x[m]);
+  }
+  __syncthreads();
+}
+
 // PACKED 0: user layout; 1: packed float4 cells (four images); 2: half of a
 // packed half8 cell (fp16 storage, use_h8): this CTA's four rows are images
 // 4g .. 4g+3, i.e. the low or high 8 bytes of group g / 2's cells.
+//
+// Passes (P = 2^logP points, two complex sequences z = row_a + i row_b):
+//   forward DIF: the first pass reads the rows from global memory (the upper
+//   half is the zero padding: not read, first layer pruned), the middle
+//   passes run in shared memory, the last pass multiplies by the response
+//   (slot q holds frequency brev(q)) before storing;
+//   inverse DIT: the middle passes in shared memory, the last pass crops to
+//   det_count, scales and writes the result from registers.
+// Twiddles are staged in shared memory once per CTA (the L1 gathers of a
+// global table made the kernel LSU-bound: ncu r2c, mio_throttle).
 template <class TIn, class TOut, int PACKED>
 __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
                                                                 int nd, int P, int logP,
@@ -51,12 +116,11 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
                                                                 const float2* __restrict__ tw, float scale,
                                                                 TOut* __restrict__ out, float4* __restrict__ packed) {
   extern __shared__ float2 fsm[];
-  float2* za = fsm;      // rows q=0 (re) and q=1 (im), swizzled slots (swz)
-  float2* zb = fsm + P;  // rows q=2 (re) and q=3 (im)
+  float2* za = fsm;          // rows q=0 (re) and q=1 (im), swizzled slots (fft_swz)
+  float2* tws = fsm + 2 * P;  // P/2 twiddles
   const int a = blockIdx.x;
   const int64_t g = blockIdx.y;
   const int shift = 32 - logP;
-  // ---- load (zero pad), natural order
   const TIn* rows[4];
   bool valid[4];
 #pragma unroll
@@ -65,53 +129,80 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
     valid[q] = b < batch;
     rows[q] = in + (valid[q] ? (b * na + a) * int64_t(nd) : 0);
   }
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (k < nd) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (valid[q]) v[q] = ld_f32(rows[q] + k);
+  for (int k = threadIdx.x; k < P / 2; k += blockDim.x) tws[k] = __ldg(tw + k);
+  __syncthreads();
+  auto sm_load = [&](int seq, int i, int) { return za[seq * P + fft_swz(i)]; };
+  auto sm_store = [&](int seq, int i, int, float2 v) { za[seq * P + fft_swz(i)] = v; };
+  // sequence seq = rows 2 seq (re) and 2 seq + 1 (im); zero beyond det_count
+  // (selects, not rows[2 * seq]: a dynamic index would put the arrays in local memory)
+  auto gl_load = [&](int seq, int i, int) {
+    float re = 0.f, im = 0.f;
+    if (i < nd) {
+      const bool vre = seq ? valid[2] : valid[0], vim = seq ? valid[3] : valid[1];
+      const TIn* pre = seq ? rows[2] : rows[0];
+      const TIn* pim = seq ? rows[3] : rows[1];
+      if (vre) re = ld_f32(pre + i);
+      if (vim) im = ld_f32(pim + i);
     }
-    za[fft_swz(k)] = make_float2(v[0], v[1]);
-    zb[fft_swz(k)] = make_float2(v[2], v[3]);
-  }
-  __syncthreads();
-  fft_dif_seq(fsm, 2, P, logP, tw);
-  // ---- multiply by the real, even response; slot q holds frequency brev(q)
-  for (int q = threadIdx.x; q < P; q += blockDim.x) {
-    const int f = int(__brev(unsigned(q)) >> shift);
+    return make_float2(re, im);
+  };
+  // ---- forward DIF (natural -> bit-reversed), fft_dif_seq's pass order
+  const int r0 = logP % 3 == 0 ? 3 : logP % 3;  // the short pass first, at the widest stride
+  int lh = logP - r0;
+  const bool single = lh == 0;  // one pass (P <= 8): it both reads the rows and applies the response
+  auto mul_store = [&](int seq, int i, int, float2 v) {
+    const int f = int(__brev(unsigned(i)) >> shift);
     const float h = __ldg(resp + (f <= P / 2 ? f : P - f));
-    const int sq = fft_swz(q);
-    const float2 x = za[sq], y = zb[sq];
-    za[sq] = make_float2(x.x * h, x.y * h);
-    zb[sq] = make_float2(y.x * h, y.y * h);
+    za[seq * P + fft_swz(i)] = make_float2(v.x * h, v.y * h);
+  };
+  if (r0 == 1) {
+    if (single) filter_pass<1, true, false, true>(logP, lh, tws, gl_load, mul_store);
+    else filter_pass<1, true, false, true>(logP, lh, tws, gl_load, sm_store);
+  } else if (r0 == 2) {
+    if (single) filter_pass<2, true, false, true>(logP, lh, tws, gl_load, mul_store);
+    else filter_pass<2, true, false, true>(logP, lh, tws, gl_load, sm_store);
+  } else {
+    if (single) filter_pass<3, true, false, true>(logP, lh, tws, gl_load, mul_store);
+    else filter_pass<3, true, false, true>(logP, lh, tws, gl_load, sm_store);
   }
-  __syncthreads();
-  ifft_dit_seq(fsm, 2, P, logP, tw);
-  // ---- crop, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
+  while (lh >= 3) {
+    lh -= 3;
+    if (lh == 0)
+      filter_pass<3, true, false, false>(logP, lh, tws, sm_load, mul_store);
+    else
+      filter_pass<3, true, false, false>(logP, lh, tws, sm_load, sm_store);
+  }
+  // ---- inverse DIT (bit-reversed -> natural), conjugate twiddles; the last
+  // pass crops, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
   const float inv = 1.0f / float(P);
-  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    const float2 x = za[fft_swz(k)], y = zb[fft_swz(k)];
-    const float v[4] = {(x.x * inv) * scale, (x.y * inv) * scale, (y.x * inv) * scale, (y.y * inv) * scale};
+  auto out_store = [&](int seq, int i, int, float2 v) {
+    if (i >= nd) return;
+    const float v0 = (v.x * inv) * scale, v1 = (v.y * inv) * scale;
     if (PACKED == 2) {
-      // four halves: exactly the values the float4 path narrows through fp16
-      const __half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]), h2 = __float2half_rn(v[2]),
-                   h3 = __float2half_rn(v[3]);
-      const uint2 bits = make_uint2(unsigned(__half_as_ushort(h0)) | (unsigned(__half_as_ushort(h1)) << 16),
-                                    unsigned(__half_as_ushort(h2)) | (unsigned(__half_as_ushort(h3)) << 16));
-      reinterpret_cast<uint2*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + k) * 2 + (g & 1)] = bits;
+      // two halves of this CTA's four: exactly the values the float4 path narrows through fp16
+      const unsigned bits = unsigned(__half_as_ushort(__float2half_rn(v0))) |
+                            (unsigned(__half_as_ushort(__float2half_rn(v1))) << 16);
+      reinterpret_cast<unsigned*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + i) * 4 + (g & 1) * 2 + seq] = bits;
     } else if (PACKED == 1) {
       // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows
       // to the storage precision first (sino_filter.cpp:123, 126-128)
-      packed[(g * na + a) * int64_t(nd) + k] =
-          make_float4(float(st_cast<TOut>(v[0])), float(st_cast<TOut>(v[1])), float(st_cast<TOut>(v[2])),
-                      float(st_cast<TOut>(v[3])));
+      reinterpret_cast<float2*>(packed)[((g * na + a) * int64_t(nd) + i) * 2 + seq] =
+          make_float2(float(st_cast<TOut>(v0)), float(st_cast<TOut>(v1)));
     } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (valid[q]) out[((g * kPack + q) * na + a) * int64_t(nd) + k] = st_cast<TOut>(v[q]);
+      const bool vre = seq ? valid[2] : valid[0], vim = seq ? valid[3] : valid[1];
+      if (vre) out[((g * kPack + 2 * seq) * na + a) * int64_t(nd) + i] = st_cast<TOut>(v0);
+      if (vim) out[((g * kPack + 2 * seq + 1) * na + a) * int64_t(nd) + i] = st_cast<TOut>(v1);
     }
+  };
+  int lq = 0;
+  for (; lq + 3 <= logP; lq += 3) {
+    if (lq + 3 == logP)
+      filter_pass<3, false, true, false>(logP, lq, tws, sm_load, out_store);
+    else
+      filter_pass<3, false, true, false>(logP, lq, tws, sm_load, sm_store);
   }
+  if (logP - lq == 2) filter_pass<2, false, true, false>(logP, lq, tws, sm_load, out_store);
+  if (logP - lq == 1) filter_pass<1, false, true, false>(logP, lq, tws, sm_load, out_store);
 }
 
 template <class F>
@@ -131,7 +222,7 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   const int P = int(f.padded);
   int logP = 0;
   while ((1 << logP) < P) ++logP;
-  const size_t smem = size_t(2) * P * sizeof(float2);
+  const size_t smem = (size_t(2) * P + size_t(P) / 2) * sizeof(float2);  // two sequences + twiddles
   const float scale = float(M_PI / (2.0 * double(n_angles)));  // sino_filter.cpp:108
   dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
   dispatch(dtype, [&](auto tag) {
