@@ -73,7 +73,7 @@ __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, 
         if (m & (1 << bit)) continue;
         const int q = m | (1 << bit);
         const int k = lo + ((m & ((1 << bit) - 1)) << lh);
-        const float2 w = tw[k << (logn - lh - 1 - bit)];
+        const float2 w = __ldg(tw + ((1 << (lh + bit)) - 1) + k);  // stage lh + bit, entry k (= W^(k << ...))
         const float2 u = x[m];
         if (DIF) {
           if (ZERO_TOP && l == 0) {  // v = 0: u + v = u, (u - v) W = u W
@@ -107,8 +107,9 @@ __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, 
 //   (slot q holds frequency brev(q)) before storing;
 //   inverse DIT: the middle passes in shared memory, the last pass crops to
 //   det_count, scales and writes the result from registers.
-// Twiddles are staged in shared memory once per CTA (the L1 gathers of a
-// global table made the kernel LSU-bound: ncu r2c, mio_throttle).
+// Twiddles come from a per-stage table (the stage's entries consecutive), so
+// a warp's twiddle loads are coalesced; the strided gathers of the flat table
+// made the kernel LSU-bound (ncu r2c: L1TEX 96 %, mio_throttle).
 template <class TIn, class TOut, int PACKED>
 __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
                                                                 int nd, int P, int logP,
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
                                                                 const float2* __restrict__ tw, float scale,
                                                                 TOut* __restrict__ out, float4* __restrict__ packed) {
   extern __shared__ float2 fsm[];
-  float2* za = fsm;          // rows q=0 (re) and q=1 (im), swizzled slots (fft_swz)
-  float2* tws = fsm + 2 * P;  // P/2 twiddles
+  float2* za = fsm;  // rows q=0 (re) and q=1 (im), swizzled slots (fft_swz)
+  const float2* tws = tw;  // per-stage twiddle table (plan.cpp build_filter): consecutive per butterfly lane
   const int a = blockIdx.x;
   const int64_t g = blockIdx.y;
   const int shift = 32 - logP;
@@ -129,8 +130,6 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
     valid[q] = b < batch;
     rows[q] = in + (valid[q] ? (b * na + a) * int64_t(nd) : 0);
   }
-  for (int k = threadIdx.x; k < P / 2; k += blockDim.x) tws[k] = __ldg(tw + k);
-  __syncthreads();
   auto sm_load = [&](int seq, int i, int) { return za[seq * P + fft_swz(i)]; };
   auto sm_store = [&](int seq, int i, int, float2 v) { za[seq * P + fft_swz(i)] = v; };
   // sequence seq = rows 2 seq (re) and 2 seq + 1 (im); zero beyond det_count
@@ -222,7 +221,7 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   const int P = int(f.padded);
   int logP = 0;
   while ((1 << logP) < P) ++logP;
-  const size_t smem = (size_t(2) * P + size_t(P) / 2) * sizeof(float2);  // two sequences + twiddles
+  const size_t smem = size_t(2) * P * sizeof(float2);  // two sequences
   const float scale = float(M_PI / (2.0 * double(n_angles)));  // sino_filter.cpp:108
   dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
   dispatch(dtype, [&](auto tag) {
@@ -233,7 +232,7 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
     allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FILTER, st);
     kern<<<grid, kFilterThreads, smem, st>>>(static_cast<const T*>(in), batch, int(n_angles), int(f.det_count), P,
-                                             logP, f.d_response.as<float>(), f.d_twiddle.as<float2>(), scale,
+                                             logP, f.d_response.as<float>(), f.d_twiddle_stage.as<float2>(), scale,
                                              static_cast<T*>(out), packed_out);
   });
   RK_CUDA(cudaGetLastError());

@@ -400,8 +400,18 @@ void build_filter(Filter& f, int kind, int64_t det_count) {
     double ang = 2.0 * M_PI * double(k) / double(n);
     tw[size_t(k)] = make_float2(float(std::cos(ang)), float(-std::sin(ang)));
   }
+  // the same twiddles regrouped per radix-2 stage s (offset 2^s - 1, 2^s entries: W^(k n / 2^(s+1))),
+  // so a stage's butterflies read consecutive entries (filter.cu) instead of a strided gather
+  int logn = 0;
+  while ((int64_t(1) << logn) < n) ++logn;
+  std::vector<float2> tws(static_cast<size_t>(std::max<int64_t>(n - 1, 1)));
+  for (int st = 0; st < logn; ++st)
+    for (int64_t k = 0; k < (int64_t(1) << st); ++k)
+      tws[size_t((int64_t(1) << st) - 1 + k)] = tw[size_t(k << (logn - 1 - st))];
   if (f.device < 0) return;  // host-only filter (response inspection without a GPU)
   rk::set_device(f.device);
+  f.d_twiddle_stage.reserve(tws.size() * sizeof(float2));
+  RK_CUDA(cudaMemcpy(f.d_twiddle_stage.ptr, tws.data(), tws.size() * sizeof(float2), cudaMemcpyHostToDevice));
   f.d_response.reserve(f.response_f.size() * sizeof(float));
   f.d_twiddle.reserve(tw.size() * sizeof(float2));
   RK_CUDA(cudaMemcpy(f.d_response.ptr, f.response_f.data(), f.response_f.size() * sizeof(float),

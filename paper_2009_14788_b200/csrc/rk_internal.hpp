@@ -180,6 +180,7 @@ struct Filter {
   std::vector<float> response_f;  // same, float (sino_filter.cpp:89)
   DeviceBuffer d_response;        // float, padded/2+1
   DeviceBuffer d_twiddle;         // float2, padded/2 (forward twiddles)
+  DeviceBuffer d_twiddle_stage;   // float2, padded - 1: the same values per radix-2 stage (filter.cu)
   HostPipeline pipe;              // rk_filter_sinogram_host
   std::mutex mu;
 };
