@@ -57,7 +57,8 @@ constexpr int kFilterThreads = 256;
 template <int R, bool DIF, bool CONJ, bool ZERO_TOP, class Load, class Store>
 __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, Load load, Store store) {
   const int gl = logn - R;
-  for (int t = threadIdx.x; t < (2 << gl); t += blockDim.x) {
+#pragma unroll 4
+  for (int t = threadIdx.x; t < (2 << gl); t += kFilterThreads) {
     const int seq = t >> gl, g = t & ((1 << gl) - 1);
     const int lo = g & ((1 << lh) - 1), hi = g >> lh;
     const int i0 = lo + (hi << (lh + R));
@@ -110,12 +111,19 @@ __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, 
 // Twiddles come from a per-stage table (the stage's entries consecutive), so
 // a warp's twiddle loads are coalesced; the strided gathers of the flat table
 // made the kernel LSU-bound (ncu r2c: L1TEX 96 %, mio_throttle).
-template <class TIn, class TOut, int PACKED>
+//
+// LOGP > 0 fixes the transform size at compile time (the common sizes,
+// launch_filter): every stride, shift and loop bound folds into the code,
+// which the issue-bound passes need (ncu r2d: 79 % issue active); LOGP = 0
+// takes the size at run time.
+template <class TIn, class TOut, int PACKED, int LOGP>
 __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
-                                                                int nd, int P, int logP,
+                                                                int nd, int P_rt, int logP_rt,
                                                                 const float* __restrict__ resp,
                                                                 const float2* __restrict__ tw, float scale,
                                                                 TOut* __restrict__ out, float4* __restrict__ packed) {
+  const int logP = LOGP ? LOGP : logP_rt;
+  const int P = LOGP ? (1 << LOGP) : P_rt;
   extern __shared__ float2 fsm[];
   float2* za = fsm;  // rows q=0 (re) and q=1 (im), swizzled slots (fft_swz)
   const float2* tws = tw;  // per-stage twiddle table (plan.cpp build_filter): consecutive per butterfly lane
@@ -164,6 +172,7 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
     if (single) filter_pass<3, true, false, true>(logP, lh, tws, gl_load, mul_store);
     else filter_pass<3, true, false, true>(logP, lh, tws, gl_load, sm_store);
   }
+#pragma unroll
   while (lh >= 3) {
     lh -= 3;
     if (lh == 0)
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
     }
   };
   int lq = 0;
+#pragma unroll
   for (; lq + 3 <= logP; lq += 3) {
     if (lq + 3 == logP)
       filter_pass<3, false, true, false>(logP, lq, tws, sm_load, out_store);
@@ -226,9 +236,21 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
   dispatch(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = packed_out ? filter_kernel<T, T, 1> : filter_kernel<T, T, 0>;
+    // compile-time sizes for P = 2^9 .. 2^13 (det_count 129 .. 4096), run-time size otherwise
+    auto pick = [&](auto packed_tag) {
+      constexpr int PK = decltype(packed_tag)::value;
+      switch (logP) {
+        case 9: return filter_kernel<T, T, PK, 9>;
+        case 10: return filter_kernel<T, T, PK, 10>;
+        case 11: return filter_kernel<T, T, PK, 11>;
+        case 12: return filter_kernel<T, T, PK, 12>;
+        case 13: return filter_kernel<T, T, PK, 13>;
+        default: return filter_kernel<T, T, PK, 0>;
+      }
+    };
+    auto kern = packed_out ? pick(std::integral_constant<int, 1>{}) : pick(std::integral_constant<int, 0>{});
     if constexpr (std::is_same<T, __half>::value)
-      if (packed_out && use_h8(dtype, batch)) kern = filter_kernel<T, T, 2>;
+      if (packed_out && use_h8(dtype, batch)) kern = pick(std::integral_constant<int, 2>{});
     allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FILTER, st);
     kern<<<grid, kFilterThreads, smem, st>>>(static_cast<const T*>(in), batch, int(n_angles), int(f.det_count), P,
