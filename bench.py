@@ -503,12 +503,12 @@ def main():
     return 0
 
 
-def first_call_latency(rk, _lib, g, gpu, img1):
+def first_call_latency(rk, _lib, g, gpu, img1, reps=3):
     """One-shot latency of the reference-shaped call (projector.cpp:228-236: a stateless forward):
     a new plan + the first rk_forward_host of one image (host buffers, copies included), with the
     forward schedule planned from scratch ("cold": empty plan cache), read from the on-disk plan
     cache ("warm_cache": a new process projecting a geometry seen before), and a second call on the
-    same plan ("steady")."""
+    same plan ("steady").  Median of `reps` rounds, each with a fresh cache directory."""
     import tempfile
 
     from paper_2009_14788_b200.projector import Plan
@@ -516,29 +516,33 @@ def first_call_latency(rk, _lib, g, gpu, img1):
     na, nd = g.n_angles, g.det_count
     out = np.empty((1, na, nd), np.float32)
     saved = os.environ.get("RK_PLAN_CACHE")
-    res = {}
+    runs = {"cold": [], "warm_cache": [], "steady": []}
     try:
-        os.environ["RK_PLAN_CACHE"] = tempfile.mkdtemp(prefix="rk_bench_cache_")
-        for key in ("cold", "warm_cache"):
-            t0 = time.perf_counter()
-            p = Plan(g, 1.0, gpu)
-            _lib.check(_lib.lib.rk_forward_host(p.handle, _lib.RK_F32, ctypes_void(img1.ctypes.data), 1,
-                                                ctypes_void(out.ctypes.data)))
-            res[key] = 1e3 * (time.perf_counter() - t0)
-            if key == "warm_cache":
-                assert p.info()["schedule_from_cache"]
+        for _ in range(reps):
+            os.environ["RK_PLAN_CACHE"] = tempfile.mkdtemp(prefix="rk_bench_cache_")
+            for key in ("cold", "warm_cache"):
                 t0 = time.perf_counter()
+                p = Plan(g, 1.0, gpu)
                 _lib.check(_lib.lib.rk_forward_host(p.handle, _lib.RK_F32, ctypes_void(img1.ctypes.data), 1,
                                                     ctypes_void(out.ctypes.data)))
-                res["steady"] = 1e3 * (time.perf_counter() - t0)
-            del p
+                runs[key].append(1e3 * (time.perf_counter() - t0))
+                assert p.info()["schedule_from_cache"] == (key == "warm_cache")
+                if key == "warm_cache":
+                    t0 = time.perf_counter()
+                    _lib.check(_lib.lib.rk_forward_host(p.handle, _lib.RK_F32, ctypes_void(img1.ctypes.data), 1,
+                                                        ctypes_void(out.ctypes.data)))
+                    runs["steady"].append(1e3 * (time.perf_counter() - t0))
+                del p
     finally:
         if saved is None:
             os.environ.pop("RK_PLAN_CACHE", None)
         else:
             os.environ["RK_PLAN_CACHE"] = saved
+    res = {k: statistics.median(v) for k, v in runs.items()}
+    res["runs"] = {k: [round(x, 2) for x in v] for k, v in runs.items()}
     res["what"] = ("new plan + first rk_forward_host of 1 image (pageable host buffers): schedule planned (cold), "
-                   "read from the plan cache (warm_cache); steady = the next call on the same plan")
+                   "read from the plan cache (warm_cache); steady = the next call on the same plan; median of "
+                   f"{reps} rounds (fresh cache directory each)")
     return res
 
 
