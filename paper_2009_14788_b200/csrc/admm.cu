@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 
 #include "rk_internal.hpp"
@@ -60,7 +61,7 @@ __global__ void assemble_kernel(const float4* __restrict__ bp, const float* __re
 
 // z2 = clamp_min(f + u2, 0); u2 = u2 + (f - z2); all_finite(f), all_finite(u2) (admm.cpp:152-159)
 __global__ void positivity_kernel(const float4* __restrict__ f, float4* __restrict__ z2, float4* __restrict__ u2,
-                                  int64_t batch, int64_t plane, int64_t total, int* flag, int iteration) {
+                                  int64_t batch, int64_t plane, int64_t total, int* flag, const int* iteration) {
   for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t g = idx / plane;
@@ -77,9 +78,12 @@ __global__ void positivity_kernel(const float4* __restrict__ f, float4* __restri
     }
     z2[idx] = make_float4(z[0], z[1], z[2], z[3]);
     u2[idx] = make_float4(u[0], u[1], u[2], u[3]);
-    if (bad) atomicMin(flag, iteration);
+    if (bad) atomicMin(flag, *iteration);
   }
 }
+
+// the end of an outer iteration: advance the device iteration counter
+__global__ void next_iteration_kernel(int* iteration) { ++*iteration; }
 
 template <class T>
 __global__ void convert_kernel(const float* __restrict__ in, int64_t n, T* __restrict__ out) {
@@ -103,7 +107,7 @@ void admm_init(Admm& a, const void* d_sino, const std::vector<double>& threshold
   a.sino.reserve(size_t(G * p.na * p.nd) * sizeof(float4));
   a.user.reserve(2 * size_t(a.batch * npx) * sizeof(float));
   a.coeff.reserve(2 * size_t(a.batch * K * npx) * sizeof(float));
-  const size_t thresh_bytes = (size_t(K) * sizeof(float) + 255) / 256 * 256;
+  const size_t thresh_bytes = (size_t(K) * sizeof(float) + 255) / 256 * 256;  // then flags[2], iteration
   a.small.reserve(thresh_bytes + 256 + cg_scalar_bytes(a.batch));
   char* pk = a.packed.as<char>();
   a.F = reinterpret_cast<float4*>(pk);
@@ -118,6 +122,7 @@ void admm_init(Admm& a, const void* d_sino, const std::vector<double>& threshold
   a.u1 = a.z1 + a.batch * K * npx;
   a.thresh = a.small.as<float>();
   a.flags = reinterpret_cast<int*>(a.small.as<char>() + thresh_bytes);
+  a.iter_dev = a.flags + 2;
   a.cg_scalars = a.small.as<char>() + thresh_bytes + 256;
   // thresh = scale(w, p0 / p1) in fp64 (computed by the caller), read as float by shrink (admm.cpp:135, :53-82)
   std::vector<float> th(static_cast<size_t>(K));
@@ -138,29 +143,101 @@ void admm_init(Admm& a, const void* d_sino, const std::vector<double>& threshold
   a.failed = -1;
 }
 
-int64_t admm_iterate(Admm& a, int64_t n, cudaStream_t st) {
+Admm::~Admm() {
+  if (graph) cudaGraphExecDestroy(graph);
+  if (graph_in) cudaEventDestroy(graph_in);
+  if (graph_out) cudaEventDestroy(graph_out);
+  if (graph_stream) cudaStreamDestroy(graph_stream);
+}
+
+namespace {
+
+// One outer iteration (admm.cpp:146-160), all on `st`.
+void outer_iteration(Admm& a, cudaStream_t st) {
   Plan& p = *a.plan;
   Shearlet& sh = *a.sh;
   const int64_t G = groups_of(a.batch), P = p.s + 2, img_plane = P * P, total = G * img_plane;
-  for (int64_t i = 0; i < n; ++i) {
-    const int it = int(a.iterations_done + i);
-    shearlet_admm_synth(sh, a.z1, a.u1, a.batch, a.shU, st);
-    {
-      KernelTimer t(RK_KERNEL_SOLVER, st);
-      assemble_kernel<<<grid_for(total, 256), 256, 0, st>>>(a.BP, a.shU, a.Z2, a.U2, a.batch, int(p.s), total, a.p0f,
-                                                            a.p1f, a.CGY);
-      RK_CUDA(cudaGetLastError());
+  shearlet_admm_synth(sh, a.z1, a.u1, a.batch, a.shU, st);
+  {
+    KernelTimer t(RK_KERNEL_SOLVER, st);
+    assemble_kernel<<<grid_for(total, 256), 256, 0, st>>>(a.BP, a.shU, a.Z2, a.U2, a.batch, int(p.s), total, a.p0f,
+                                                          a.p1f, a.CGY);
+    RK_CUDA(cudaGetLastError());
+  }
+  cg_packed(p, a.batch, a.CGY, a.F, a.inner, 0.0, &a.sys, a.work, a.sino.as<float4>(), a.cg_scalars, a.flags + 1, st);
+  unpack_images(RK_F32, a.F, a.batch, p.s, a.fU, st);
+  shearlet_admm_shrink(sh, a.fU, a.batch, a.z1, a.u1, a.thresh, a.flags, a.iter_dev, st);
+  {
+    KernelTimer t(RK_KERNEL_SOLVER, st);
+    positivity_kernel<<<grid_for(total, 256), 256, 0, st>>>(a.F, a.Z2, a.U2, a.batch, img_plane, total, a.flags,
+                                                            a.iter_dev);
+    next_iteration_kernel<<<1, 1, 0, st>>>(a.iter_dev);
+    RK_CUDA(cudaGetLastError());
+  }
+}
+
+bool graph_current(const Admm& a) {
+  return a.graph && a.graph_key[0] == a.sh->work_a.ptr && a.graph_key[1] == a.sh->work_b.ptr;
+}
+
+// Captures outer_iteration on the ADMM's own stream (the caller's may be the
+// legacy default stream, which cannot be captured).  Every buffer the
+// iteration touches must already have its size: the caller runs one eager
+// iteration first.
+void capture(Admm& a) {
+  if (a.graph) {
+    cudaGraphExecDestroy(a.graph);
+    a.graph = nullptr;
+  }
+  if (!a.graph_stream) {
+    RK_CUDA(cudaStreamCreateWithFlags(&a.graph_stream, cudaStreamNonBlocking));
+    RK_CUDA(cudaEventCreateWithFlags(&a.graph_in, cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&a.graph_out, cudaEventDisableTiming));
+  }
+  cudaGraph_t g = nullptr;
+  RK_CUDA(cudaStreamBeginCapture(a.graph_stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    outer_iteration(a, a.graph_stream);
+  } catch (...) {
+    cudaStreamEndCapture(a.graph_stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    throw;
+  }
+  RK_CUDA(cudaStreamEndCapture(a.graph_stream, &g));
+  const cudaError_t e = cudaGraphInstantiate(&a.graph, g, 0);
+  cudaGraphDestroy(g);
+  RK_CUDA(e);
+  a.graph_key[0] = a.sh->work_a.ptr;
+  a.graph_key[1] = a.sh->work_b.ptr;
+}
+
+}  // namespace
+
+int64_t admm_iterate(Admm& a, int64_t n, cudaStream_t st) {
+  // the device counter starts at the number of iterations done (flags name the outer iteration)
+  const int start = int(a.iterations_done);
+  RK_CUDA(cudaMemcpyAsync(a.iter_dev, &start, sizeof(int), cudaMemcpyHostToDevice, st));
+  // Graph replay unless the per-kernel event timing is on (its records are per launch) or
+  // RK_ADMM_GRAPH=0; identical kernels and arguments either way, so identical results.
+  const char* ge = std::getenv("RK_ADMM_GRAPH");
+  const bool use_graph = !profiling_enabled() && !(ge && ge[0] == '0');
+  int64_t i = 0;
+  if (use_graph && n > 0) {
+    if (!graph_current(a)) {
+      outer_iteration(a, st);  // sizes every scratch buffer before the capture
+      ++i;
+      capture(a);  // also when n == 1: the observer's one-iteration calls replay it next time
     }
-    cg_packed(p, a.batch, a.CGY, a.F, a.inner, 0.0, &a.sys, a.work, a.sino.as<float4>(), a.cg_scalars, a.flags + 1,
-              st);
-    unpack_images(RK_F32, a.F, a.batch, p.s, a.fU, st);
-    shearlet_admm_shrink(sh, a.fU, a.batch, a.z1, a.u1, a.thresh, a.flags, it, st);
-    {
-      KernelTimer t(RK_KERNEL_SOLVER, st);
-      positivity_kernel<<<grid_for(total, 256), 256, 0, st>>>(a.F, a.Z2, a.U2, a.batch, img_plane, total, a.flags, it);
-      RK_CUDA(cudaGetLastError());
+    if (i < n) {
+      RK_CUDA(cudaEventRecord(a.graph_in, st));
+      RK_CUDA(cudaStreamWaitEvent(a.graph_stream, a.graph_in, 0));
+      for (; i < n; ++i) RK_CUDA(cudaGraphLaunch(a.graph, a.graph_stream));
+      RK_CUDA(cudaEventRecord(a.graph_out, a.graph_stream));
+      RK_CUDA(cudaStreamWaitEvent(st, a.graph_out, 0));
     }
   }
+  for (; i < n; ++i) outer_iteration(a, st);
   a.iterations_done += n;
   int h[2] = {INT_MAX, INT_MAX};
   RK_CUDA(cudaMemcpyAsync(h, a.flags, sizeof(h), cudaMemcpyDeviceToHost, st));

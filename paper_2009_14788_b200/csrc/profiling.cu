@@ -59,6 +59,7 @@ KernelTimer::~KernelTimer() {
 }
 
 void profiling_enable(bool on) { g_timing.store(on); }
+bool profiling_enabled() { return g_timing.load(); }
 
 void allow_dynamic_smem(const void* func, size_t bytes) {
   if (bytes <= 48 * 1024) return;

@@ -208,7 +208,7 @@ void shearlet_backward(Shearlet& sp, int dtype, const void* coeff, int64_t batch
 // ADMM fusions (fp32, user layouts): z1 = shrink(SH(f) + u1, thresh_k), u1 += SH(f) - z1
 // (non-finite u1 -> atomicMin(flag, iteration)); image = SH'(z1 - u1)
 void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1, float* u1, const float* thresh,
-                          int* flag, int iteration, cudaStream_t st);
+                          int* flag, const int* iteration, cudaStream_t st);
 void shearlet_admm_synth(Shearlet& sp, const float* z1, const float* u1, int64_t batch, float* image,
                          cudaStream_t st);
 
@@ -247,7 +247,20 @@ struct Admm {
   float* u1 = nullptr;
   float* thresh = nullptr;
   int* flags = nullptr;  // [0] divergence iteration, [1] CG non-positive curvature
+  int* iter_dev = nullptr;  // the current outer iteration, advanced on the device (graph replays)
   void* cg_scalars = nullptr;
+  // One outer iteration captured as a CUDA graph and replayed (admm_iterate):
+  // a batch-1 iteration is ~460 short launches.  Valid while the shearlet
+  // plan's scratch keeps its addresses (graph_key); replayed on graph_stream,
+  // ordered after / before the caller's stream by events.
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t graph_in = nullptr, graph_out = nullptr;
+  const void* graph_key[2] = {nullptr, nullptr};
+  Admm() = default;
+  Admm(const Admm&) = delete;
+  Admm& operator=(const Admm&) = delete;
+  ~Admm();
 };
 // bp = A'y, zero state; thresholds[k] = w_k p0 / p1 in fp64, used as float (admm.cpp:129-140)
 void admm_init(Admm& a, const void* d_sino, const std::vector<double>& thresholds, cudaStream_t st);
@@ -342,6 +355,7 @@ class KernelTimer {
 // concurrent launch that needs more (calls from several host threads).
 void allow_dynamic_smem(const void* func, size_t bytes);
 void profiling_enable(bool on);
+bool profiling_enabled();
 void profiling_read(rk_kernel_stats* out, bool reset);
 double probe_smem_bandwidth(int device);
 

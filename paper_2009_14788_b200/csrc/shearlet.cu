@@ -100,8 +100,8 @@ struct AdmmStore {
   float* z1 = nullptr;  // null: plain store
   float* u1 = nullptr;
   const float* thresh = nullptr;  // per coefficient, float((p0/p1) w_k)
-  int* flag = nullptr;            // atomicMin(iteration) when u1 turns non-finite
-  int iteration = 0;
+  int* flag = nullptr;            // atomicMin(*iteration) when u1 turns non-finite
+  const int* iteration = nullptr;  // device counter: the outer iteration (admm.cu; graph-replay safe)
 };
 
 // soft(a, b) = sign(a) max(|a| - b, 0) (admm.cpp:46-51)
@@ -117,7 +117,7 @@ __device__ __forceinline__ void admm_update(const AdmmStore& a, int64_t gi, int 
   const float un = __fadd_rn(u, __fsub_rn(c, z));
   a.z1[gi] = z;
   a.u1[gi] = un;
-  if (!isfinite(un)) atomicMin(a.flag, a.iteration);
+  if (!isfinite(un)) atomicMin(a.flag, *a.iteration);
 }
 
 // ---------------------------------------------------------------- row passes
@@ -674,7 +674,7 @@ void shearlet_backward(Shearlet& sp, int dtype, const void* coeff, int64_t batch
 }
 
 void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1, float* u1, const float* thresh,
-                          int* flag, int iteration, cudaStream_t st) {
+                          int* flag, const int* iteration, cudaStream_t st) {
   AdmmStore a;
   a.z1 = z1;
   a.u1 = u1;

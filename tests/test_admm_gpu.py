@@ -239,3 +239,30 @@ def test_parameter_validation(rk, cuda):
         rk.admm_reconstruct(op, plan, torch.zeros(1, 11, s, device=cuda))
     with pytest.raises(rk.ValidationError, match="does not match plan grid"):
         rk.admm_reconstruct(op, rk.make_plan(8, 8, [0.5]), y)
+
+
+def test_graph_replay_equals_direct_launches(rk, port, cuda, monkeypatch):
+    """admm.cu replays one captured outer iteration as a CUDA graph (RK_ADMM_GRAPH, default on):
+    the same kernels with the same arguments, so the result is bit-identical to direct launches —
+    for a one-shot run, for an observer stepping one iteration per call (capture after the first,
+    replays after), and when a divergence must still name its outer iteration."""
+    s = 32
+    g = rk.make_parallel(s, limited_angles(24))
+    op = rk.projector_operator(g)
+    y = rk.forward(g, dev(phantom(port, s, np.float32), cuda))
+    plan = rk.make_plan(s, s, [0.5, 0.5])
+    p = rk.AdmmParams(outer_iterations=6, inner_cg_iterations=12)
+    seen = {}
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RK_ADMM_GRAPH", mode)
+        out[mode] = host(rk.admm_reconstruct(op, plan, y, p))
+        its = []
+        seen[mode] = host(rk.admm_reconstruct(op, plan, y, p, lambda it, st: its.append(it)))
+        assert its == list(range(6))
+    assert np.array_equal(out["1"], out["0"])
+    assert np.array_equal(seen["1"], seen["0"]) and np.array_equal(seen["1"], out["0"])
+    monkeypatch.setenv("RK_ADMM_GRAPH", "1")
+    with pytest.raises(rk.DivergenceError) as e:
+        rk.admm_reconstruct(op, plan, y, rk.AdmmParams(outer_iterations=5, p0=1e30))
+    assert e.value.iteration == 0
