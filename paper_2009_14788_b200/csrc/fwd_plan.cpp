@@ -32,7 +32,9 @@
 #include <cstring>
 #include <functional>
 #include <stdexcept>
+#include <mutex>
 #include <thread>
+#include <utility>
 
 #include "rk_internal.hpp"
 
@@ -205,6 +207,119 @@ void verify_forward_schedule(const Plan& p, const std::vector<float4>& ray_geom,
   }
 }
 
+// Exact model of the forward kernel's shared-memory load wavefronts for one
+// image group under the final schedule: every CTA's lanes replayed in
+// lockstep per chunk iteration (the kernel's own fp32 positions, tap orders,
+// orientation and pitch), each quarter warp's LDS.128 costing the largest
+// number of distinct 16-byte cells that share one of the 8 slots.  Returns
+// {modelled, conflict-free}.  RK_PLAN_MODEL=1 (diagnostics: ncu measures
+// l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld per launch = groups x this).
+std::pair<double, double> model_wavefronts(const Plan& p, const std::vector<float4>& ray_geom,
+                                           const std::vector<float4>& ray_aux) {
+  const ForwardSchedule& F = p.fwd;
+  const int64_t nd = p.nd;
+  std::atomic<int> next{0};
+  std::mutex mu;
+  double tot = 0.0, ideal = 0.0;
+  auto work = [&]() {
+    double my_tot = 0.0, my_ideal = 0.0;
+    std::vector<int> base(256), n(256), m(256), mend(256);
+    std::vector<float> pxc(256), pyc(256), hx(256), hy(256);
+    std::vector<float4> G(256), X(256);
+    std::vector<char> ok(256);
+    for (int cta; (cta = next.fetch_add(1)) < int(F.cta.size());) {
+      const int4 cfg = F.cta[size_t(cta)];
+      const int lq = (cfg.z >> 3) & 3;
+      const int2* wa = &F.warps[size_t(cta) * 8];
+      for (int t = 0; t < 256; ++t) {
+        int slot = t >> 5, k;
+        if (lq == 0) {
+          k = wa[t >> 5].y + (t & 31);
+        } else {
+          const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
+          const int cg = (t >> 3) & ((4 << lq) - 1), ag = t >> (lq + 5);
+          slot = (ag << lq) + aq;
+          k = wa[0].y + cg * (8 >> lq) + cq;
+        }
+        const int a = wa[slot].x;
+        ok[size_t(t)] = a >= 0 && k < nd;
+        m[size_t(t)] = 0;
+        n[size_t(t)] = 0;
+        if (!ok[size_t(t)]) continue;
+        const size_t r = size_t(int64_t(a) * nd + k);
+        G[size_t(t)] = ray_geom[r];
+        X[size_t(t)] = ray_aux[r];
+        std::memcpy(&n[size_t(t)], &X[size_t(t)].y, 4);
+      }
+      for (int c = 0; c < cfg.y; ++c) {
+        const int4 bx = F.boxes[size_t(cfg.x + c)];
+        const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, pitch = bx.z & 0xffff;
+        const bool tr = ((bx.z >> 16) & 1) != 0;
+        const int swap = (bx.z >> 17) & 3;
+        float tend;
+        std::memcpy(&tend, &bx.w, 4);
+        int iters = 0;
+        for (int t = 0; t < 256; ++t) {
+          mend[size_t(t)] = m[size_t(t)];
+          if (!ok[size_t(t)]) continue;
+          const float t0 = X[size_t(t)].z, inv_h = X[size_t(t)].w;
+          const int nn = n[size_t(t)];
+          mend[size_t(t)] = std::isinf(tend) ? nn
+                                             : std::min(std::max(int(std::ceil(std::fma(tend - t0, inv_h, -0.5f))), 0), nn);
+          iters = std::max(iters, mend[size_t(t)] - m[size_t(t)]);
+          const float4 g = G[size_t(t)];
+          pxc[size_t(t)] = (tr ? g.y : g.x) - float(c0);
+          pyc[size_t(t)] = (tr ? g.x : g.y) - float(r0);
+          hx[size_t(t)] = tr ? g.w : g.z;
+          hy[size_t(t)] = tr ? g.z : g.w;
+        }
+        for (int q = 0; q < iters; ++q) {
+          for (int qw = 0; qw < 256; qw += 8) {
+            int used = 0;
+            for (int l = 0; l < 8; ++l) {
+              const int t = qw + l;
+              const int mm = m[size_t(t)] + q;
+              if (!ok[size_t(t)] || mm >= mend[size_t(t)]) continue;
+              const float tt = float(mm) + 0.5f;
+              const float px = std::fma(tt, hx[size_t(t)], pxc[size_t(t)]);
+              const float py = std::fma(tt, hy[size_t(t)], pyc[size_t(t)]);
+              const int j = int(std::floor(px)), i = int(std::floor(py));
+              const bool odd = (t & 1) != 0, rs = swap == 1 && odd, cs = swap == 2 && odd;
+              base[size_t(used++)] = (i * pitch + j + (rs ? pitch : 0) + (cs ? 1 : 0)) |
+                                     ((cs ? 1 : 0) << 30) | ((rs ? 1 : 0) << 29);
+            }
+            if (!used) continue;
+            my_ideal += 4.0;
+            for (int tap = 0; tap < 4; ++tap) {
+              int addr[8], cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, worst = 1;
+              for (int u = 0; u < used; ++u) {
+                const int b = base[size_t(u)];
+                const bool cs = (b >> 30) & 1, rs = (b >> 29) & 1;
+                const int a0 = b & ((1 << 29) - 1);
+                const int dX = cs ? -1 : 1, dY = rs ? -pitch : pitch;
+                addr[u] = a0 + ((tap & 1) ? dX : 0) + ((tap & 2) ? dY : 0);
+                bool first = true;
+                for (int v = 0; v < u; ++v) first &= addr[v] != addr[u];
+                if (first) worst = std::max(worst, ++cnt[addr[u] & 7]);
+              }
+              my_tot += worst;
+            }
+          }
+        }
+        for (int t = 0; t < 256; ++t) m[size_t(t)] = mend[size_t(t)];
+      }
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    tot += my_tot;
+    ideal += my_ideal;
+  };
+  const int nthreads = std::max(1, int(std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nthreads; ++t) pool.emplace_back(work);
+  for (auto& th : pool) th.join();
+  return {tot, ideal};
+}
+
 }  // namespace
 
 void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<float4>& ray_geom,
@@ -240,6 +355,11 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   // Checks and diagnostics of the final schedule (planned or from the cache).
   auto finish = [&]() {
     if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
+    if (const char* me = std::getenv("RK_PLAN_MODEL"); me && me[0] == '1') {
+      const auto w = model_wavefronts(p, ray_geom, ray_aux);
+      std::fprintf(stderr, "[rk] forward schedule: modelled shared-memory load wavefronts per image group %.0f "
+                   "(%.4fx conflict-free)\n", w.first, w.first / std::max(w.second, 1.0));
+    }
     if (std::getenv("RK_DEBUG_PLAN")) {
       int64_t ntr = 0;
       for (const int4& c : F.cta) ntr += c.z & 1;
@@ -275,6 +395,19 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   const double t_lo = (fan ? p.g.source_distance : 0.0) - R - 1.0;
   const double t_hi = (fan ? p.g.source_distance : 0.0) + R + 1.0;
   const int64_t nkb = (nd + 31) / 32;  // 32-cell detector blocks
+  // Each chunk's layout is chosen from `refine_steps` of the kernel's own lockstep iterations in
+  // the chunk (lane m = m_start + q), evenly spaced: cfg2 modelled wavefronts 1.272x -> 1.242x of
+  // conflict-free, forward 9.46 -> 9.26 ms (r2).  RK_FWD_REFINE_STEPS=0: the r1 planner's three
+  // sampled t's.  (The model: RK_PLAN_MODEL=1, within 0.1 % of ncu's count.)
+  const char* prs = std::getenv("RK_FWD_REFINE_STEPS");
+  const int refine_steps = prs ? std::max(0, std::atoi(prs)) : 6;
+  const char* pml = std::getenv("RK_FWD_MAXLEN");  // experiment: cap on a chunk's t-length
+  const double max_len = pml ? std::atof(pml) : 48.0;
+  const char* pcl = std::getenv("RK_FWD_CTA_LOCKSTEP");  // experiment: "q,step" lockstep samples per t
+  const bool cta_lockstep = pcl != nullptr;
+  int cta_q = 1, cta_qstep = 0;
+  if (pcl) std::sscanf(pcl, "%d,%d", &cta_q, &cta_qstep);
+  cta_q = std::max(1, cta_q);
   const char* pce = std::getenv("RK_FWD_CHUNK_LAYOUT");
   const bool per_chunk_layout = !(pce && pce[0] == '0');
   int64_t budget = F.box_budget;
@@ -325,6 +458,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     while (t < t_hi) {
       bool placed = false;
       for (double len : {48.0, 40.0, 32.0, 24.0, 16.0, 12.0, 8.0, 6.0, 4.0, 3.0, 2.0}) {
+        if (len > max_len && len > 2.0) continue;
         const double tb = std::min(t + len, t_hi);
         Box b = box_of(wa, t, tb);
         if (b.empty()) {
@@ -413,8 +547,9 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     double best = 1e300;
     for (int mapping = 0; mapping < (full8 ? 4 : 1); ++mapping) {
       sim.clear();
-      for (int st = 0; st < 8; ++st) {
-        const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st) / 7.0);
+      for (int st = 0; st < 8 * cta_q; ++st) {
+        const double tt = t_lo + (t_hi - t_lo) * (0.06 + 0.88 * double(st / cta_q) / 7.0);
+        const int qoff = (st % cta_q) * cta_qstep;  // lockstep iterations after a chunk start at tt
         for (int w = 0; w < 8; ++w)
           for (int l = 0; l < 32; ++l) {
             Pt q{NAN, NAN};
@@ -424,9 +559,10 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
             if (a >= 0 && kk < nd) {
               const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
               if (ry.n > 0 && tt >= ry.t0 && tt <= ry.t1) {
-                const double m = std::floor((tt - ry.t0) / ry.h);
+                double m = std::floor((tt - ry.t0) / ry.h);
+                if (cta_lockstep) m = std::ceil((tt - ry.t0) / ry.h - 0.5) + double(qoff);
                 const double t = ry.t0 + (m + 0.5) * ry.h;
-                q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
+                if (m < double(ry.n)) q = to_pixel(ry.ox + t * ry.dx, ry.oy + t * ry.dy, half);
               }
             }
             sim.push_back(q);
@@ -452,7 +588,41 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     const int mp = cp.mapping;
     Refine refine = [&](double ta, double tb, int* tr_o, int* res_o, int* sw_o) {
       csim.clear();
-      for (int st = 0; st < 3; ++st) {
+      if (refine_steps > 0) {
+        // the kernel's lockstep iterations of this chunk (lane m = m_start + q), `refine_steps`
+        // of them evenly spaced: the samples whose t lies in [ta, tb)
+        int iters = 0;
+        std::vector<int64_t> ms(256, 0), me(256, 0);
+        std::vector<const RayD*> rl(256, nullptr);
+        for (int w = 0; w < 8; ++w)
+          for (int l = 0; l < 32; ++l) {
+            int a;
+            int64_t kk;
+            lane_ray(mp, w, l, a, kk);
+            if (a < 0 || kk >= nd) continue;
+            const RayD& ry = rays[size_t(int64_t(a) * nd + kk)];
+            if (ry.n == 0) continue;
+            const int t = w * 32 + l;
+            rl[size_t(t)] = &ry;
+            ms[size_t(t)] = std::min<int64_t>(std::max<int64_t>(int64_t(std::ceil((ta - ry.t0) / ry.h - 0.5)), 0), ry.n);
+            me[size_t(t)] = std::min<int64_t>(std::max<int64_t>(int64_t(std::ceil((tb - ry.t0) / ry.h - 0.5)), 0), ry.n);
+            iters = std::max<int>(iters, int(me[size_t(t)] - ms[size_t(t)]));
+          }
+        const int ns = std::min(iters, refine_steps);
+        for (int st = 0; st < ns; ++st) {
+          const int64_t q = ns == 1 ? iters / 2 : int64_t(st) * (iters - 1) / (ns - 1);
+          for (int t = 0; t < 256; ++t) {
+            Pt pt{NAN, NAN};
+            const RayD* ry = rl[size_t(t)];
+            if (ry && ms[size_t(t)] + q < me[size_t(t)]) {
+              const double tt = ry->t0 + (double(ms[size_t(t)] + q) + 0.5) * ry->h;
+              pt = to_pixel(ry->ox + tt * ry->dx, ry->oy + tt * ry->dy, half);
+            }
+            csim.push_back(pt);
+          }
+        }
+      }
+      for (int st = 0; refine_steps == 0 && st < 3; ++st) {
         const double tt = ta + (tb - ta) * (0.2 + 0.3 * st);
         for (int w = 0; w < 8; ++w)
           for (int l = 0; l < 32; ++l) {
