@@ -129,6 +129,54 @@ void conflict_costs(const std::vector<Pt>& lanes_at_step, bool transposed, doubl
     for (int r = 0; r < 8; ++r) cost[sw][r] = double(acc[sw][r]);
 }
 
+// Per-lane tap order of a chunk (box record z bits 17-30, kernels.cu): bit
+// l - 1 of the low 7 bits set = lane l of every quarter warp (l = 1..7) loads
+// the bottom row first, bit l - 1 of the high 7 bits = the right column first
+// (lane 0 never flips: flipping all lanes only permutes the four loads).  The
+// r1 tap orders are the odd-lane patterns.
+constexpr int kOddLanes = 0x55;  // lanes 1, 3, 5, 7
+inline int order_of_swap(int sw) { return sw == 1 ? kOddLanes : sw == 2 ? kOddLanes << 7 : 0; }
+inline bool order_row(int order, int lane8) { return lane8 != 0 && ((order >> (lane8 - 1)) & 1); }
+inline bool order_col(int order, int lane8) { return lane8 != 0 && ((order >> (6 + lane8)) & 1); }
+
+// conflict_costs for one arbitrary per-lane tap order: out[r] = the sum over
+// quarter warps and the four taps of the worst slot, pitch residue r.
+__attribute__((target_clones("avx2", "default")))
+void order_costs(const std::vector<Pt>& lanes_at_step, bool transposed, int order, V8& out) {
+  out = V8{0, 0, 0, 0, 0, 0, 0, 0};
+  const int nw = int(lanes_at_step.size()) / 32;
+  for (int w = 0; w < nw; ++w)
+    for (int q = 0; q < 32; q += 8) {
+      int32_t bi[8], bj[8];
+      int lane_of[8];
+      int used = 0;
+      for (int l = 0; l < 8; ++l) {
+        const Pt& pt = lanes_at_step[size_t(w * 32 + q + l)];
+        if (std::isnan(pt.px)) continue;
+        const double cx = transposed ? pt.py : pt.px, cy = transposed ? pt.px : pt.py;
+        bj[used] = int32_t(std::floor(cx));
+        bi[used] = int32_t(std::floor(cy));
+        lane_of[used] = l;
+        ++used;
+      }
+      if (!used) continue;
+      for (int tap = 0; tap < 4; ++tap) {
+        uint64_t key[8];
+        V8 cnt = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int u = 0; u < used; ++u) {
+          const int rb = tap >> 1, cb = tap & 1;
+          const int32_t ti = bi[u] + (order_row(order, lane_of[u]) ? 1 - rb : rb);
+          const int32_t tj = bj[u] + (order_col(order, lane_of[u]) ? 1 - cb : cb);
+          key[u] = (uint64_t(uint32_t(ti)) << 32) | uint32_t(tj);
+          bool first = true;
+          for (int v = 0; v < u; ++v) first &= key[v] != key[u];
+          if (first) cnt += kSlots.inc[((ti & 7) << 3) | (tj & 7)];
+        }
+        out += worst_slot(cnt);
+      }
+    }
+}
+
 // Conflict-free reference for conflict_cost: one wavefront per quarter warp
 // and tap with at least one active lane.
 double ideal_cost(const std::vector<Pt>& lanes_at_step) {
@@ -255,7 +303,7 @@ std::pair<double, double> model_wavefronts(const Plan& p, const std::vector<floa
         const int4 bx = F.boxes[size_t(cfg.x + c)];
         const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, pitch = bx.z & 0xffff;
         const bool tr = ((bx.z >> 16) & 1) != 0;
-        const int swap = (bx.z >> 17) & 3;
+        const int order = (bx.z >> 17) & 0x3fff;
         float tend;
         std::memcpy(&tend, &bx.w, 4);
         int iters = 0;
@@ -284,7 +332,7 @@ std::pair<double, double> model_wavefronts(const Plan& p, const std::vector<floa
               const float px = std::fma(tt, hx[size_t(t)], pxc[size_t(t)]);
               const float py = std::fma(tt, hy[size_t(t)], pyc[size_t(t)]);
               const int j = int(std::floor(px)), i = int(std::floor(py));
-              const bool odd = (t & 1) != 0, rs = swap == 1 && odd, cs = swap == 2 && odd;
+              const bool rs = order_row(order, t & 7), cs = order_col(order, t & 7);
               base[size_t(used++)] = (i * pitch + j + (rs ? pitch : 0) + (cs ? 1 : 0)) |
                                      ((cs ? 1 : 0) << 30) | ((rs ? 1 : 0) << 29);
             }
@@ -401,6 +449,11 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   // sampled t's.  (The model: RK_PLAN_MODEL=1, within 0.1 % of ncu's count.)
   const char* prs = std::getenv("RK_FWD_REFINE_STEPS");
   const int refine_steps = prs ? std::max(0, std::atoi(prs)) : 6;
+  // RK_FWD_ORDER_DESCENT=n: n passes of coordinate descent over per-lane tap orders per chunk.
+  // Off: the exact model gives 0.4-0.6 % fewer wavefronts (cfg2 1.2418x -> 1.2357x, cfg3 1.3367x ->
+  // 1.3291x) for 4x the planning time (r2).
+  const char* pod = std::getenv("RK_FWD_ORDER_DESCENT");
+  const int order_descent = pod ? std::max(0, std::atoi(pod)) : 0;
   const char* pml = std::getenv("RK_FWD_MAXLEN");  // experiment: cap on a chunk's t-length
   const double max_len = pml ? std::atof(pml) : 48.0;
   const char* pcl = std::getenv("RK_FWD_CTA_LOCKSTEP");  // experiment: "q,step" lockstep samples per t
@@ -451,7 +504,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   // refine (optional): per-chunk layout {tr, residue, swap} for the chunk
   // [t, tb] with box b; the CTA-wide layout when it returns false or its box
   // would not fit.
-  using Refine = std::function<bool(double, double, int*, int*, int*)>;
+  using Refine = std::function<bool(double, double, int*, int*, int*)>;  // -> tr, residue, tap order
   auto chunk_cta = [&](const int2* wa, bool tr, int residue, int swap, std::vector<int4>* out, int64_t* staged,
                        int64_t* max_cells, bool* any_tr, const Refine& refine) -> bool {
     double t = t_lo;
@@ -472,21 +525,21 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
         if (rows * pitch > budget && len > 2.0) continue;
         if (rows * pitch > budget) return false;
         bool ctr = tr;
-        int cswap = swap;
-        int ctr_i = tr, cres = residue, csw = swap;
-        if (refine && refine(t, tb, &ctr_i, &cres, &csw)) {
+        int corder = order_of_swap(swap);
+        int ctr_i = tr, cres = residue, cord = corder;
+        if (refine && refine(t, tb, &ctr_i, &cres, &cord)) {
           const int64_t rr = ctr_i ? b.cols : b.rows, cc = ctr_i ? b.rows : b.cols;
           const int pp = pitch_for(cc, cres);
-          if (rr * pp <= budget) ctr = ctr_i != 0, cswap = csw, rows = rr, cols = cc, pitch = pp;
+          if (rr * pp <= budget) ctr = ctr_i != 0, corder = cord, rows = rr, cols = cc, pitch = pp;
         }
         if (out) {
           const int64_t r0 = ctr ? b.c0 : b.r0, c0 = ctr ? b.r0 : b.c0;
           float tend = tb >= t_hi ? INFINITY : float(tb);
           int tbits;
           std::memcpy(&tbits, &tend, 4);
-          // pitch | orientation << 16 | tap order << 17 (kernels.cu)
+          // pitch | orientation << 16 | per-lane tap order << 17 (kernels.cu)
           out->push_back(make_int4(int(r0 | (c0 << 16)), int(rows | (cols << 16)),
-                                   pitch | (int(ctr) << 16) | (cswap << 17), tbits));
+                                   pitch | (int(ctr) << 16) | (corder << 17), tbits));
         }
         if (any_tr) *any_tr |= ctr;
         if (staged) *staged += rows * cols;
@@ -642,6 +695,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           }
       }
       double bc = 1e300;
+      int bsw = 0;
       for (int tr = 0; tr < 2; ++tr) {
         double costs[3][8];
         conflict_costs(csim, tr == 1, costs);
@@ -650,8 +704,29 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
             // ties keep the CTA-wide layout (no needless switches)
             const bool same = tr == cp.tr && res == cp.residue && sw == cp.swap;
             const double c = costs[sw][res] * (same ? 1.0 : 1.0 + 1e-3);
-            if (c < bc) bc = c, *tr_o = tr, *res_o = res, *sw_o = sw;
+            if (c < bc) bc = c, *tr_o = tr, *res_o = res, bsw = sw;
           }
+      }
+      *sw_o = order_of_swap(bsw);
+      if (bc < 1e300 && order_descent > 0) {
+        // per-lane tap orders: coordinate descent over the 14 order bits from the best
+        // odd-lane order, each candidate at its best pitch residue
+        int order = *sw_o, res = *res_o;
+        V8 cv;
+        order_costs(csim, *tr_o == 1, order, cv);
+        uint32_t best = cv[res];
+        for (int pass = 0; pass < order_descent; ++pass) {
+          bool improved = false;
+          for (int bit = 0; bit < 14; ++bit) {
+            const int cand = order ^ (1 << bit);
+            order_costs(csim, *tr_o == 1, cand, cv);
+            for (int r = 0; r < 8; ++r)
+              if (cv[r] < best) best = cv[r], order = cand, res = r, improved = true;
+          }
+          if (!improved) break;
+        }
+        *sw_o = order;
+        *res_o = res;
       }
       return bc < 1e300;
     };

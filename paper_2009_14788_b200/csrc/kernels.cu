@@ -271,12 +271,12 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
   // Per-chunk layout chosen by the planner against bank conflicts (box record
-  // z = pitch | orientation << 16 | tap order << 17): chunks of transposed
-  // orientation stage the transposed packed image with x and y swapped, and
-  // odd lanes issue the bottom row first (tap order 1) or the right column
-  // first (2).  Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA) (rowB,colB);
-  // the weights follow the same order, so no value is moved between registers.
-  const bool odd = (threadIdx.x & 1) != 0;
+  // z = pitch | orientation << 16 | per-lane tap order << 17): chunks of
+  // transposed orientation stage the transposed packed image with x and y
+  // swapped, and lanes flagged by the tap order issue the bottom row first or
+  // the right column first.  Loads L1..L4 = (rowA,colA) (rowA,colB) (rowB,colA)
+  // (rowB,colB); the weights follow the same order, so no value is moved
+  // between registers.
   float4 G = make_float4(0.f, 0.f, 0.f, 0.f), X = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     G = __ldg(ray_geom + r);
@@ -319,8 +319,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const int4 bx = __ldg(bxs + c);  // CTA-uniform
     const int r0 = bx.x & 0xffff, c0 = bx.x >> 16, rows = bx.y & 0xffff, cols = bx.y >> 16, pitch = bx.z & 0xffff;
     const bool tr = ((bx.z >> 16) & 1) != 0;
-    const int swap = (bx.z >> 17) & 3;
-    const bool rs = swap == 1 && odd, cs = swap == 2 && odd;
+    // per-lane tap order (fwd_plan.cpp order_row / order_col): lane l of each quarter
+    // warp loads the bottom row first / the right column first
+    const int order = (bx.z >> 17) & 0x3fff, l8 = threadIdx.x & 7;
+    const bool rs = l8 != 0 && ((order >> (l8 - 1)) & 1), cs = l8 != 0 && ((order >> (l8 + 6)) & 1);
     const int dX = cs ? -1 : 1;
     const float px0 = tr ? G.y : G.x, py0 = tr ? G.x : G.y;
     const float hx = tr ? G.w : G.z, hy = tr ? G.z : G.w;

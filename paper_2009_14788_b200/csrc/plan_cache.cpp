@@ -29,7 +29,7 @@ namespace rk {
 namespace {
 
 // Bump whenever fwd_plan.cpp's decisions change (the key then misses).
-constexpr uint32_t kPlannerVersion = 3;
+constexpr uint32_t kPlannerVersion = 4;
 constexpr char kMagic[4] = {'R', 'K', 'F', 'S'};
 
 void put(std::vector<unsigned char>& b, const void* d, size_t n) {
@@ -114,7 +114,7 @@ std::vector<unsigned char> schedule_cache_key(const Plan& p) {
   put(k, p.angles.data(), p.angles.size() * sizeof(double));
   put_v(k, p.fwd.box_budget);
   for (const char* e : {"RK_FWD_CHUNK_LAYOUT", "RK_FWD_BOX", "RK_FWD_ORDER", "RK_FWD_REFINE_STEPS", "RK_FWD_MAXLEN",
-                        "RK_FWD_CTA_LOCKSTEP"})
+                        "RK_FWD_CTA_LOCKSTEP", "RK_FWD_ORDER_DESCENT"})
     put_env(k, e);
   return k;
 }
