@@ -194,3 +194,29 @@ def test_adjoint_defect_fixture(golden):
 def test_batched_phantom_helper(port):
     b = batched_phantom(port, 16, 3)
     assert b.shape == (3, 16, 16) and np.allclose(b[2], 3 * b[0], atol=1e-6)
+
+
+def test_reference_isa_builds_agree_bitwise():
+    """oracle/Makefile builds the reference for x86-64-v3 and -v4 (AVX-512); RefOracle picks the
+    highest the host runs.  -ffp-contract=off and no fast-math: the two must agree bit for bit."""
+    import os
+
+    import numpy as np
+    import pytest
+
+    from oracle import REF_SO, REF_SO_V4, Geom, RefOracle, _cpu_flags, _V4_FLAGS
+
+    if not (os.path.exists(REF_SO) and os.path.exists(REF_SO_V4)):
+        pytest.skip("reference oracle builds absent")
+    if not all(f in _cpu_flags() for f in _V4_FLAGS):
+        pytest.skip("host lacks AVX-512")
+    a, b = RefOracle(REF_SO), RefOracle(REF_SO_V4)
+    x = a.shepp_logan(48)
+    x = np.concatenate([x, a.rng_uniform(3, 48 * 48).reshape(1, 48, 48)])
+    for g in (Geom("parallel", 48, a.angles_linspace(0.0, np.pi, 37), 61),
+              Geom("fanbeam", 48, a.angles_linspace(0.0, 2 * np.pi, 29), source_distance=80.0)):
+        ya, yb = a.forward(g, x), b.forward(g, x)
+        assert np.array_equal(ya, yb)
+        assert np.array_equal(a.backprojection(g, ya), b.backprojection(g, ya))
+        if g.kind == "parallel":
+            assert np.array_equal(a.fbp(g, ya), b.fbp(g, ya))
