@@ -170,6 +170,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n"
@@ -543,6 +546,22 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
 #pragma unroll
     for (int q = 0; q < (H8 ? kPackH8 : 1); ++q) acc8[r][q] = 0.f;
 
+  // Packed cells (float4 / half8) are staged by TMA bulk copies: one per angle
+  // (the in-detector part of its window, a contiguous run of 16-byte cells),
+  // issued by the thread that derived the window, completing on an mbarrier
+  // that warp 0's 32 lanes arrive on each pass; the out-of-detector cells are
+  // zero-filled by the CTA.  This keeps the staging off the LSU (r1 loaded
+  // the cells through L1 into registers and stored them).  LANE (lane 0 of
+  // each cell) still stages through registers.
+  __shared__ unsigned long long win_bar;
+  if constexpr (!LANE) {
+    if (tid == 0) {
+      mbar_init(&win_bar, 32);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  unsigned win_phase = 0;
   for (int a0 = 0; a0 < na; a0 += chunk) {
     const int nac = min(chunk, na - a0);
     // ---- per-angle constants, fp64 (one thread per angle)
@@ -596,18 +615,36 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
         ws_s[tid] = ws;
       }
       cst[tid] = k;
+      if constexpr (!LANE) {
+        // this angle's in-detector cells [k0, k1) of the window [ws, ws + window)
+        const int ws = ws_s[tid];
+        const int k0 = max(ws, 0), k1 = min(ws + window, nd);
+        const unsigned bytes = k1 > k0 ? unsigned(k1 - k0) * 16u : 0u;
+        // the previous pass read (generic proxy) what this copy overwrites (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive_expect_tx(&win_bar, bytes);
+        if (bytes)
+          tma_bulk_g2s(win + tid * window + (k0 - ws), sg + int64_t(a0 + tid) * nd + k0, bytes, &win_bar);
+      }
+    } else if (!LANE && tid < 32) {
+      mbar_arrive(&win_bar);
     }
     __syncthreads();
-    // ---- stage the detector windows (coalesced 16-byte cells)
+    // ---- stage the detector windows (16-byte cells; zero outside [0, det_count))
     for (int e = tid; e < nac * window; e += NT) {
       const int q = e / window, cidx = e - q * window;
       const int k = ws_s[q] + cidx;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k >= 0 && k < nd) v = __ldg(sg + int64_t(a0 + q) * nd + k);
-      if constexpr (LANE)
+      if constexpr (LANE) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k >= 0 && k < nd) v = __ldg(sg + int64_t(a0 + q) * nd + k);
         win[e] = v.x;
-      else
-        win[e] = v;
+      } else {
+        if (k < 0 || k >= nd) win[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if constexpr (!LANE) {
+      mbar_wait(&win_bar, win_phase);
+      win_phase ^= 1u;
     }
     __syncthreads();
     // ---- accumulate
