@@ -343,3 +343,36 @@ def test_host_only_plan_teardown_leaves_no_cuda_error(rk, oracle, cuda):
     torch.cuda.synchronize()
     assert torch.cuda.current_device() == before
     assert rel_l2(host(sino), oracle.forward(ogeom(g), host(x))) <= TOL32
+
+
+@pytest.mark.parametrize("kind", ["parallel", "fanbeam"])
+def test_device_plan_from_cache_projects_bitwise_equal(rk, oracle, cuda, tmp_path, monkeypatch, kind):
+    """A device plan whose forward schedule comes from the on-disk plan cache (plan_cache.cpp)
+    launches exactly what a freshly planned one does: same digest, bit-identical sinograms."""
+    from paper_2009_14788_b200.projector import Plan
+
+    s = 96
+    if kind == "parallel":
+        g = rk.make_parallel(s, rk.angles_linspace(0.0, np.pi, 70))
+    else:
+        g = rk.make_fanbeam(s, rk.angles_linspace(0.0, 2 * np.pi, 70), 1.4 * s)
+    x = dev(batched_phantom(oracle, s, 6), cuda)
+    monkeypatch.setenv("RK_PLAN_CACHE", "off")
+    fresh = Plan(g, 1.0, cuda.index or 0)
+    h_fresh = fresh.prepare()
+    monkeypatch.setenv("RK_PLAN_CACHE", str(tmp_path))
+    Plan(g, 1.0, cuda.index or 0).prepare()  # plans and stores
+    cached = Plan(g, 1.0, cuda.index or 0)
+    assert cached.prepare() == h_fresh and cached.info()["schedule_from_cache"]
+    import ctypes
+
+    from paper_2009_14788_b200 import _lib
+
+    outs = []
+    for p in (fresh, cached):
+        y = torch.empty(6, 70, g.det_count, device=cuda)
+        _lib.check(_lib.lib.rk_forward(p.handle, _lib.RK_F32, ctypes.c_void_p(x.data_ptr()), 6,
+                                       ctypes.c_void_p(y.data_ptr()), None))
+        outs.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])

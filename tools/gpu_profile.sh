@@ -23,3 +23,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"for
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"forward_kernel|backproject_kernel" -s 2 -c 2 -o gpurun_out/prof_${TAG}_fan python tools/prof_step.py fan512 2 128 > gpurun_out/ncu_${TAG}_fan.log 2>&1; tail -1 gpurun_out/ncu_${TAG}_fan.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"forward_kernel|backproject_kernel" -s 2 -c 2 -o gpurun_out/prof_${TAG}_h8 python tools/prof_step.py par512 2 128 f16 > gpurun_out/ncu_${TAG}_h8.log 2>&1; tail -1 gpurun_out/ncu_${TAG}_h8.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"filter_kernel" -s 1 -c 1 -o gpurun_out/prof_${TAG}_filter python tools/prof_fbp.py 1024 2 > gpurun_out/ncu_${TAG}_filter.log 2>&1; tail -1 gpurun_out/ncu_${TAG}_filter.log
+timeout 600 python tools/shard_probe.py par512 > gpurun_out/shard_probe_${TAG}_par.json 2>&1; tail -c 400 gpurun_out/shard_probe_${TAG}_par.json; echo
+timeout 600 python tools/b1_probe.py > gpurun_out/b1_probe_${TAG}.json 2>&1; tail -c 300 gpurun_out/b1_probe_${TAG}.json; echo
+timeout 600 python tools/fbp_probe.py > gpurun_out/fbp_probe_${TAG}.json 2>&1; tail -c 300 gpurun_out/fbp_probe_${TAG}.json; echo
