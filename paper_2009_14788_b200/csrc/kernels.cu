@@ -490,16 +490,20 @@ constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 // WIDE (small batches, float4 cells): 512 threads x 2 pixels per tile, so the
 // few tiles of one or two image groups still fill the SMs with warps; per pixel
 // the operations and their order are the 256-thread kernel's (bit-identical).
-template <int KIND, class TOut, bool LANE, bool H8 = false, bool WIDE = false>
-__global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
-                                  (LANE || H8 || WIDE) ? 2 : (KIND == kBpFan64 ? 3 : 4))
+// NARROW (float4 cells, parallel / fan fp32 map): 128 threads x 8 pixels per
+// tile, seven CTAs per SM: the per-angle constants are read once per eight
+// pixels instead of four, and 1,036 resident CTAs hold a four-group batch's
+// 1,024 tiles in one wave; per pixel the same operations (bit-identical).
+template <int KIND, class TOut, bool LANE, bool H8 = false, bool WIDE = false, bool NARROW = false>
+__global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kBpThreads,
+                                  NARROW ? 7 : (LANE || H8 || WIDE) ? 2 : (KIND == kBpFan64 ? 3 : 4))
     backproject_kernel(
     const float4* __restrict__ sino, int s, int na, int nd, double spacing, double source_distance,
     double det_distance, const double2* __restrict__ trig, const int* __restrict__ tile_window, int cells,
     int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
   using Cell = typename std::conditional<LANE, float, float4>::type;
-  constexpr int RPT = (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
+  constexpr int RPT = NARROW ? 7 : (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
   constexpr int NT = kTile * kTile / RPT;         // threads
   extern __shared__ float4 smem_raw[];
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
@@ -667,6 +671,12 @@ __global__ void __launch_bounds__((LANE || H8 || WIDE) ? 512 : kBpThreads,
         int pr, pc;
         pixel_of(tid, r, pr, pc);
         const float lx = float(pc), ly = float(pr);
+        if constexpr (KIND == kBpFan32 && RPT > 4) {
+          if (r > 0 && r % 4 == 0) {  // NARROW: pixels r = 4.. sit on the next row
+            nrow = k.b * ly;
+            drow = fmaf(k.d, ly, k.den00);
+          }
+        }
         float kf;
         if constexpr (KIND == kBpParallel) {
           kf = fmaf(ly, k.cy, col0);
@@ -830,6 +840,15 @@ static bool single_lane(int64_t batch) {
   return on && batch == 1;
 }
 
+// float4 backprojection as 128 threads x 8 pixels per tile (RK_BP_NARROW=0: 256 x 4)
+static bool narrow_bp() {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_BP_NARROW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // backprojection of at most kWideGroups packed groups: the 512-thread variant
 static bool wide_bp(int64_t groups) {
   static const int limit = [] {
@@ -868,8 +887,9 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
   dim3 grid(tiles, tiles, unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
   const bool lane = single_lane(batch);
   const bool wide = !lane && !h8 && wide_bp(groups_of(batch));
-  dim3 block(kTile, kTile / ((lane || h8 || wide) ? 2 : kRowsPerThread));
   const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
+  const bool narrow = !lane && !h8 && !wide && kind != kBpFan64 && narrow_bp();
+  dim3 block(kTile, kTile / (narrow ? 8 : (lane || h8 || wide) ? 2 : kRowsPerThread));
   const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
   const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
@@ -880,6 +900,9 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                      : (kind == kBpParallel ? backproject_kernel<kBpParallel, T, false>
                         : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false>
                                             : backproject_kernel<kBpFan64, T, false>);
+    if (narrow)
+      kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, false, false, true>
+                                 : backproject_kernel<kBpFan32, T, false, false, false, true>;
     if (wide)
       kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, false, true>
              : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, false, true>
