@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
     int64_t batch, TOut* __restrict__ out, BpEpilogue epi) {
   using Const = typename BpConst<KIND>::type;
   using Cell = typename std::conditional<LANE, float, float4>::type;
-  constexpr int RPT = NARROW ? 7 : (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
+  constexpr int RPT = NARROW ? 8 : (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
   constexpr int NT = kTile * kTile / RPT;         // threads
   extern __shared__ float4 smem_raw[];
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
