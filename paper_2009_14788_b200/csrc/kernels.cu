@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   using Cell = typename std::conditional<LANE, float, float4>::type;
   constexpr int RPT = NARROW ? 8 : (LANE || H8 || WIDE) ? 2 : kRowsPerThread;  // pixels (rows) per thread
   constexpr int NT = kTile * kTile / RPT;         // threads
+  static_assert(kTile % RPT == 0, "pixels per thread must divide the tile height");
   extern __shared__ float4 smem_raw[];
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
   // this tile's staged cells per angle, and as many angles per pass as fit
