@@ -165,8 +165,16 @@ void run_host_pipeline(rk::HostPipeline& pipe, int device, std::mutex& mu, int64
     if (!s) RK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   // host calls are synchronous: wait for any device-pointer call still using scratch
   if (wait_first) RK_CUDA(cudaEventSynchronize(wait_first));
-  // ~8 chunks, each a whole number of packed groups and >= 4 MB of input
-  int64_t chunk = std::max<int64_t>(rk::kPack, (batch + 7) / 8);
+  // ~8 chunks (RK_PIPE_CHUNKS), each a whole number of packed groups and >= 4 MB of input
+  static const int64_t n_chunks = [] {
+    const char* e = std::getenv("RK_PIPE_CHUNKS");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(8);
+  }();
+  static const bool use_ramp = [] {
+    const char* e = std::getenv("RK_PIPE_RAMP");
+    return !(e && e[0] == '0');
+  }();
+  int64_t chunk = std::max<int64_t>(rk::kPack, (batch + n_chunks - 1) / n_chunks);
   chunk = (chunk + rk::kPack - 1) / rk::kPack * rk::kPack;
   int64_t min_items = std::max<int64_t>(1, int64_t((4u << 20) / std::max<size_t>(in_item, 1)));
   min_items = (min_items + rk::kPack - 1) / rk::kPack * rk::kPack;
@@ -184,7 +192,7 @@ void run_host_pipeline(rk::HostPipeline& pipe, int device, std::mutex& mu, int64
   for (int64_t c = rk::kPack; c < chunk; c *= 2) ramp.push_back(c);
   int64_t ramp_total = 0;
   for (int64_t c : ramp) ramp_total += 2 * c;
-  if (!ramp.empty() && batch >= ramp_total + chunk) {
+  if (use_ramp && !ramp.empty() && batch >= ramp_total + chunk) {
     sizes = ramp;
     for (int64_t rem = batch - ramp_total; rem > 0; rem -= std::min(chunk, rem)) sizes.push_back(std::min(chunk, rem));
     sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
