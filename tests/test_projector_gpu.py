@@ -376,3 +376,45 @@ def test_device_plan_from_cache_projects_bitwise_equal(rk, oracle, cuda, tmp_pat
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+_SHAPE_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+import paper_2009_14788_b200 as rk
+y = np.load({src!r})
+out = {{}}
+for name, g in [("par", rk.make_parallel(100, rk.angles_linspace(0.0, np.pi, 37), 77, 1.3)),
+                ("par512", rk.make_parallel(64, rk.angles_linspace(0.0, np.pi, 64))),
+                ("fan", rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * np.pi, 40), 150.0))]:
+    yy = np.ascontiguousarray(y[:, :g.n_angles, :g.det_count])
+    out[name] = rk.backprojection(g, torch.from_numpy(yy).cuda()).cpu().numpy()
+np.savez({dst!r}, **out)
+"""
+
+
+def test_backprojector_thread_shapes_equal_bitwise(rk, oracle, cuda, tmp_path):
+    """The 128-thread x 8-pixel backprojector (r2 default, kernels.cu NARROW) and the r1
+    256 x 4 shape (RK_BP_NARROW=0) run the same per-pixel arithmetic: a 12-image batch
+    (three packed groups) gives identical bits for parallel beam and the fan fp32 map."""
+    import os
+    import subprocess
+    import sys
+
+    rs = np.random.default_rng(5)
+    y = rs.standard_normal((12, 64, 100)).astype(np.float32)
+    src, res = str(tmp_path / "y.npy"), {}
+    np.save(src, y)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for flag in ("1", "0"):
+        dst = str(tmp_path / f"bp{flag}.npz")
+        env = dict(os.environ, RK_BP_NARROW=flag)
+        r = subprocess.run([sys.executable, "-c", _SHAPE_SCRIPT.format(root=root, src=src, dst=dst)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(dst)
+    for name in ("par", "par512", "fan"):
+        assert np.array_equal(res["1"][name], res["0"][name]), name
+        assert np.isfinite(res["1"][name]).all()
