@@ -196,6 +196,12 @@ struct Box {
 
 inline int pitch_for(int64_t cols, int residue) { return int(cols + ((residue - cols) % 8 + 8) % 8); }
 
+// Detector cells per warp of a CTA (cfg.z bits 5-7, kernels.cu): 32 >> n.  The
+// narrow-warp fallback tiers march 16 .. 1 consecutive cells per warp (the other
+// lanes idle) for coarse detectors, whose 32 neighbouring rays are too far apart
+// for any staged box.
+inline int cells_per_warp(int cfgz) { return 32 >> ((cfgz >> 5) & 7); }
+
 // Replays the forward kernel's per-lane schedule on the host in the kernel's
 // own fp32 arithmetic (std::fma == FFMA; kernels.cu, forward_kernel) and
 // checks that every sample's four taps lie inside its chunk's staged box and
@@ -219,7 +225,7 @@ void verify_forward_schedule(const Plan& p, const std::vector<float4>& ray_geom,
         k = wa[0].y + cg * (8 >> lq) + cq;
       }
       const int a = wa[slot].x;
-      if (a < 0 || k >= nd) continue;
+      if (a < 0 || k >= nd || (lq == 0 && (t & 31) >= cells_per_warp(cfg.z))) continue;
       const size_t r = size_t(int64_t(a) * nd + k);
       const float4 G = ray_geom[r], X = ray_aux[r];
       int n;
@@ -290,7 +296,7 @@ std::pair<double, double> model_wavefronts(const Plan& p, const std::vector<floa
           k = wa[0].y + cg * (8 >> lq) + cq;
         }
         const int a = wa[slot].x;
-        ok[size_t(t)] = a >= 0 && k < nd;
+        ok[size_t(t)] = a >= 0 && k < nd && (lq != 0 || (t & 31) < cells_per_warp(cfg.z));
         m[size_t(t)] = 0;
         n[size_t(t)] = 0;
         if (!ok[size_t(t)]) continue;
@@ -418,9 +424,10 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
                    "simulated wavefronts %.3fx conflict-free\n", F.mapping_count[0], F.mapping_count[1],
                    F.mapping_count[2], F.mapping_count[3], F.sim_cost / std::max(F.sim_ideal, 1.0));
       std::fprintf(stderr,
-                   "[rk] forward schedule: CTA %d angles x %d cell blocks, %zu CTAs (%lld transposed), %zu boxes "
-                   "(%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
-                   F.shape_aa, F.shape_db, F.cta.size(), (long long)ntr, F.boxes.size(),
+                   "[rk] forward schedule: CTA %d angles x %d cell blocks of %d cells, %zu CTAs (%lld transposed), "
+                   "%zu boxes (%.1f per CTA), max box %lld cells (%.1f KB), staged texels per image %.2fM\n",
+                   F.shape_aa, F.shape_db, F.cta.empty() ? 32 : cells_per_warp(F.cta[0].z), F.cta.size(),
+                   (long long)ntr, F.boxes.size(),
                    double(F.boxes.size()) / double(std::max<size_t>(F.cta.size(), 1)), (long long)F.max_box,
                    double(F.max_box) * 16.0 / 1024.0, double(F.staged_texels) / 1e6);
     }
@@ -443,6 +450,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   const double t_lo = (fan ? p.g.source_distance : 0.0) - R - 1.0;
   const double t_hi = (fan ? p.g.source_distance : 0.0) + R + 1.0;
   const int64_t nkb = (nd + 31) / 32;  // 32-cell detector blocks
+  int cw = 32;                         // detector cells per warp of the tier being planned
   // Each chunk's layout is chosen from `refine_steps` of the kernel's own lockstep iterations in
   // the chunk (lane m = m_start + q), evenly spaced: cfg2 modelled wavefronts 1.272x -> 1.242x of
   // conflict-free, forward 9.46 -> 9.26 ms (r2).  RK_FWD_REFINE_STEPS=0: the r1 planner's three
@@ -474,7 +482,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
     for (int w = 0; w < 8; ++w) {
       if (wa[w].x < 0) continue;
-      for (int l = 0; l < 32; ++l) {
+      for (int l = 0; l < cw; ++l) {
         const int64_t kk = int64_t(wa[w].y) + l;
         if (kk >= nd) break;
         const RayD& ry = rays[size_t(int64_t(wa[w].x) * nd + kk)];
@@ -554,15 +562,16 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   };
 
   auto warps_of = [&](Shape sh) {
+    const int64_t nkb_w = (nd + cw - 1) / cw;  // cw-cell detector blocks, one per warp
     const int ctas_a = int((na + sh.aa - 1) / sh.aa);
-    const int ctas_k = int((nkb + sh.db - 1) / sh.db);
+    const int ctas_k = int((nkb_w + sh.db - 1) / sh.db);
     std::vector<int2> warps(size_t(ctas_a) * ctas_k * 8, make_int2(-1, 0));
     for (int ca = 0; ca < ctas_a; ++ca)
       for (int ck = 0; ck < ctas_k; ++ck)
         for (int w = 0; w < sh.aa * sh.db; ++w) {
           const int64_t ai = int64_t(ca) * sh.aa + w / sh.db;
           const int64_t kb = int64_t(ck) * sh.db + w % sh.db;
-          if (ai < na && kb < nkb) warps[size_t(ca * ctas_k + ck) * 8 + w] = make_int2(order[size_t(ai)], int(kb * 32));
+          if (ai < na && kb < nkb_w) warps[size_t(ca * ctas_k + ck) * 8 + w] = make_int2(order[size_t(ai)], int(kb * cw));
         }
     return warps;
   };
@@ -587,7 +596,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     // a few aligned steps of the march, in lane order.
     auto lane_ray = [&](int lq, int w, int l, int& a_out, int64_t& k_out) {
       if (lq == 0) {
-        a_out = wa[w].x;
+        a_out = l < cw ? wa[w].x : -1;  // narrow warps: lanes >= cw idle
         k_out = int64_t(wa[w].y) + l;
         return;
       }
@@ -744,7 +753,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
       std::vector<Pt> sim;
       for (int lo; (lo = next.fetch_add(4)) < ctas;)
         for (int cta = lo; cta < std::min(lo + 4, ctas); ++cta)
-          plan_cta(&warps[size_t(cta) * 8], sh.aa == 8 && sh.db == 1, plans[size_t(cta)], sim);
+          plan_cta(&warps[size_t(cta) * 8], sh.aa == 8 && sh.db == 1 && cw == 32, plans[size_t(cta)], sim);
     };
     const char* pte = std::getenv("RK_PLAN_THREADS");  // planner threads (default: all host threads)
     const int want = pte ? std::atoi(pte) : int(std::thread::hardware_concurrency());
@@ -764,18 +773,26 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   struct Tier {
     Shape sh;
     int64_t budget;
+    int cells = 32;  // detector cells per warp
   };
   // First choice: 54 KB boxes (four CTAs per SM); then 64 KB (three).
   const char* be = std::getenv("RK_FWD_BOX");
   const int64_t b0 = be ? std::max<int64_t>(512, std::atoll(be)) : F.box_budget;
   const int64_t b1 = std::max<int64_t>(b0, 4096);
-  const Tier tiers[] = {{{8, 1}, b0},     {{8, 1}, b1},     {{4, 2}, b1},     {{2, 4}, b1},
-                        {{1, 8}, b1},     {{8, 1}, 12288}, {{4, 2}, 12288}, {{4, 1}, 12288},
-                        {{2, 1}, 12288}, {{1, 1}, 12288}};
+  // Coarse detectors (spacing of several pixels) spread a warp's 32 rays over
+  // hundreds of pixels, so no box fits: then warps of 16 .. 1 consecutive
+  // cells (the other lanes idle), smallest boxes last.
+  const Tier tiers[] = {{{8, 1}, b0},        {{8, 1}, b1},        {{4, 2}, b1},        {{2, 4}, b1},
+                        {{1, 8}, b1},        {{8, 1}, 12288},    {{4, 2}, 12288},    {{4, 1}, 12288},
+                        {{2, 1}, 12288},    {{1, 1}, 12288},    {{8, 1}, b0, 16},   {{8, 1}, b0, 8},
+                        {{8, 1}, b1, 4},     {{8, 1}, 12288, 2}, {{8, 1}, 12288, 1}, {{1, 1}, 12288, 1}};
   for (const Tier& tier : tiers) {
     const Shape sh = tier.sh;
     if (sh.db > 1 && nkb < sh.db && sh.db != 8) continue;
     budget = tier.budget;
+    cw = tier.cells;
+    int ncl = 0;
+    while ((32 >> ncl) > cw) ++ncl;
     std::vector<CtaPlan> plans;
     std::vector<int2> warps = plan_shape(sh, plans);
     bool ok = true;
@@ -829,7 +846,9 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
     for (int& mc : F.mapping_count) mc = 0;
     for (size_t c = 0; c < plans.size(); ++c) {
       const CtaPlan& cp = plans[c];
-      F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()), cp.tr | (cp.swap << 1) | (cp.mapping << 3), 0);
+      // z: orientation | tap order << 1 | lane mapping << 3 | log2(32 / cells per warp) << 5 (kernels.cu)
+      F.cta[c] = make_int4(int(F.boxes.size()), int(cp.boxes.size()),
+                           cp.tr | (cp.swap << 1) | (cp.mapping << 3) | (ncl << 5), 0);
       F.sim_cost += cp.cost;
       F.sim_ideal += cp.ideal;
       F.mapping_count[cp.mapping & 3] += 1;
@@ -850,7 +869,7 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
           const int2 wa = F.warps[c * 8 + size_t(w)];
           if (wa.x < 0) continue;
           int64_t longest = 0;
-          for (int l = 0; l < 32 && int64_t(wa.y) + l < nd; ++l)
+          for (int l = 0; l < cells_per_warp(F.cta[c].z) && int64_t(wa.y) + l < nd; ++l)
             longest = std::max(longest, rays[size_t(int64_t(wa.x) * nd + wa.y + l)].n);
           work[c] += longest;
         }

@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     k = __ldg(warps + cta * (kFwdThreads / 32)).y + cg * (8 >> lq) + cq;
   }
   const int a = __ldg(warps + cta * (kFwdThreads / 32) + slot).x;
-  const bool valid = a >= 0 && k < nd;
+  // narrow-warp CTAs (coarse detectors, fwd_plan.cpp): lanes >= 32 >> n idle
+  const bool valid = a >= 0 && k < nd && (lq != 0 || lane < (32 >> ((cfg.z >> 5) & 7)));
   const int64_t r = int64_t(a) * nd + k;
   // Per-chunk layout chosen by the planner against bank conflicts (box record
   // z = pitch | orientation << 16 | per-lane tap order << 17): chunks of

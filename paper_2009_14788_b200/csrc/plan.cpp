@@ -7,6 +7,7 @@
 // appendix A.2).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <limits>
@@ -258,7 +259,9 @@ void build_plan(Plan& p) {
         int64_t& tn = tile_need[size_t(ty * tiles + tx)];
         tn = std::max(tn, we - ws + 1);
       }
-      if (!fan) break;  // parallel: footprint width is translation invariant up to floor effects
+      // every tile row, also for parallel beam: the unclipped footprint width is translation
+      // invariant, but the clip to [-2, nd + 1] is not — with a detector narrower than the
+      // image the first tile row can be clipped where another row is not (r2 stress sweep)
     }
   }
   int64_t need = 0;
@@ -279,7 +282,11 @@ void build_plan(Plan& p) {
   if (fan) {
     const double rmax = half * std::sqrt(2.0);
     const double mag = span / (g.det_spacing * (g.source_distance - rmax));
-    p.bp_fan_fp64 = !(mag <= 8.0);
+    static const double max_mag = [] {
+      const char* e = std::getenv("RK_BP_FAN32_MAXMAG");
+      return e ? std::atof(e) : 4.0;
+    }();
+    p.bp_fan_fp64 = !(mag <= max_mag);
   }
   // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to
   // 192 KB) for the widest tile; narrower tiles stage more angles per pass in

@@ -29,7 +29,7 @@ namespace rk {
 namespace {
 
 // Bump whenever fwd_plan.cpp's decisions change (the key then misses).
-constexpr uint32_t kPlannerVersion = 4;
+constexpr uint32_t kPlannerVersion = 5;  // 5: narrow-warp CTAs (cfg.z bits 5-7)
 constexpr char kMagic[4] = {'R', 'K', 'F', 'S'};
 
 void put(std::vector<unsigned char>& b, const void* d, size_t n) {

@@ -28,6 +28,10 @@ cases = [
     rk.make_parallel(96, [(i * 100.0 / 64 - 50.0) * math.pi / 180 for i in range(64)]),  # limited arc
     rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * math.pi, 64), 70.0, det_distance=300.0),  # source close
     rk.make_fanbeam(80, list(rng.uniform(0, 7, 40)), 60.0, det_distance=150.0, det_count=101),
+    # coarse detectors (cells several pixels apart): the narrow-warp fallback tiers
+    rk.make_fanbeam(128, rk.angles_linspace(0.0, 2 * math.pi, 40), 128.0, det_count=16),
+    rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * math.pi, 24), 96.0, det_count=12),
+    rk.make_parallel(128, rk.angles_linspace(0.0, math.pi, 33), 10, 14.0),
 ]
 for i in range(30):  # random geometries: sizes, angle lists, detectors, fan distances
     s = int(rng.choice([3, 17, 40, 64, 97, 131, 200]))

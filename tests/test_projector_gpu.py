@@ -418,3 +418,25 @@ def test_backprojector_thread_shapes_equal_bitwise(rk, oracle, cuda, tmp_path):
     for name in ("par", "par512", "fan"):
         assert np.array_equal(res["1"][name], res["0"][name]), name
         assert np.isfinite(res["1"][name]).all()
+
+
+@pytest.mark.parametrize("name,mk", [
+    ("fan-128-det16", lambda rk: fan(rk, 128, 40, 128.0, det_count=16)),      # spacing 16: narrow-warp tiers
+    ("fan-96-det12", lambda rk: fan(rk, 96, 24, 96.0, det_count=12)),
+    ("par-128-det10-sp14", lambda rk: par(rk, 128, 33, 10, 14.0)),
+    ("par-160-det20-sp8", lambda rk: par(rk, 160, 50, 20, 8.0)),
+    ("par-100-det35-one-angle", lambda rk: rk.make_parallel(100, [-2.8931329237874532], 35, 1.0)),
+])
+@pytest.mark.parametrize("B", [1, 5])
+def test_coarse_detector_and_narrow_detector_parity(rk, oracle, cuda, name, mk, B):
+    """Detectors much coarser than the pixels (rays several pixels apart: the forward planner's
+    narrow-warp tiers) and detectors narrower than the image (the backprojection window must
+    cover every tile row, plan.cpp) — both found by tools/stress_parity.py in r2."""
+    g = mk(rk)
+    rs = np.random.default_rng(17)
+    x = rs.uniform(0.0, 1.0, (B, g.image_size, g.image_size)).astype(np.float32)
+    f = host(rk.forward(g, dev(x, cuda)))
+    assert rel_l2(f, oracle.forward(ogeom(g), x)) <= TOL32
+    y = rs.standard_normal((B, g.n_angles, g.det_count)).astype(np.float32)
+    b = host(rk.backprojection(g, dev(y, cuda)))
+    assert rel_l2(b, oracle.backprojection(ogeom(g), y)) <= TOL32
