@@ -196,6 +196,9 @@ struct Shearlet {
   // in), and the n/2 forward twiddles; fp32 built with the plan, fp64 on first use
   DeviceBuffer d_mult2, d_twiddle;
   DeviceBuffer d_mult2_64, d_twiddle64;
+  // grids that are not a power of two (shearlet_generic.cu): natural-order
+  // pairs and the n-entry DFT table
+  DeviceBuffer g_mult2, g_twiddle, g_mult2_64, g_twiddle64;
   DeviceBuffer work_a, work_b;      // spectra scratch
   std::mutex mu;
 };
@@ -211,6 +214,23 @@ void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1
                           int* flag, const int* iteration, cudaStream_t st);
 void shearlet_admm_synth(Shearlet& sp, const float* z1, const float* u1, int64_t batch, float* image,
                          cudaStream_t st);
+// grids that are not a power of two (shearlet_generic.cu): the same transforms
+// by DFT-matrix contractions; GenericAdmm non-null = the ADMM shrink store
+inline bool shearlet_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+struct GenericAdmm {
+  float* z1 = nullptr;
+  float* u1 = nullptr;
+  const float* thresh = nullptr;
+  int* flag = nullptr;
+  const int* iteration = nullptr;
+};
+template <class C>
+void build_generic_tables(const Shearlet& sp, std::vector<C>& mult2, std::vector<C>& tw);
+void upload_shearlet_generic(Shearlet& sp);
+void shearlet_forward_generic(Shearlet& sp, int dtype, const void* image, int64_t batch, void* coeff,
+                              const GenericAdmm& admm, cudaStream_t st);
+void shearlet_backward_generic(Shearlet& sp, int dtype, const void* coeff, const void* sub, int64_t batch,
+                               void* image, cudaStream_t st);
 
 // CG system coefficients: (c0 A'A + c1 I) (solver.cu cg_packed)
 struct CgSystem {

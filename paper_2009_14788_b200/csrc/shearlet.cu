@@ -3,7 +3,7 @@
 // Re(ifft2(fft2(x) * M_k)); synthesis sums fft2(c_k) * M_k over k and takes
 // Re(ifft2(.)).  Arithmetic follows the reference's precision split
 // (shearlet.cpp:303-310): fp64 storage computes in fp64, fp32 / fp16 storage
-// in fp32; power-of-two grids.
+// in fp32; power-of-two grids (other sizes: shearlet_generic.cu).
 //
 // Layout and passes (no transposes, no bit-reversal permutes):
 //   * 2-D FFTs are a row pass and a column pass over natural [row][col]
@@ -633,6 +633,7 @@ void backward_impl(Shearlet& sp, const T* coeff, const T* sub, int64_t batch, T*
 
 void upload_shearlet(Shearlet& sp) {
   if (sp.device < 0) return;
+  if (!shearlet_pow2(sp.height)) return upload_shearlet_generic(sp);
   std::vector<float2> m2, tw;
   build_tables<float>(sp, m2, tw);
   rk::set_device(sp.device);
@@ -643,6 +644,7 @@ void upload_shearlet(Shearlet& sp) {
 }
 
 void shearlet_forward(Shearlet& sp, int dtype, const void* image, int64_t batch, void* coeff, cudaStream_t st) {
+  if (!shearlet_pow2(sp.height)) return shearlet_forward_generic(sp, dtype, image, batch, coeff, GenericAdmm{}, st);
   switch (dtype) {
     case RK_F16:
       forward_impl<__half, float>(sp, static_cast<const __half*>(image), batch, static_cast<__half*>(coeff), {}, st);
@@ -658,6 +660,7 @@ void shearlet_forward(Shearlet& sp, int dtype, const void* image, int64_t batch,
 }
 
 void shearlet_backward(Shearlet& sp, int dtype, const void* coeff, int64_t batch, void* image, cudaStream_t st) {
+  if (!shearlet_pow2(sp.height)) return shearlet_backward_generic(sp, dtype, coeff, nullptr, batch, image, st);
   switch (dtype) {
     case RK_F16:
       backward_impl<__half, float>(sp, static_cast<const __half*>(coeff), nullptr, batch, static_cast<__half*>(image), st);
@@ -675,6 +678,15 @@ void shearlet_backward(Shearlet& sp, int dtype, const void* coeff, int64_t batch
 
 void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1, float* u1, const float* thresh,
                           int* flag, const int* iteration, cudaStream_t st) {
+  if (!shearlet_pow2(sp.height)) {
+    GenericAdmm g;
+    g.z1 = z1;
+    g.u1 = u1;
+    g.thresh = thresh;
+    g.flag = flag;
+    g.iteration = iteration;
+    return shearlet_forward_generic(sp, RK_F32, f, batch, nullptr, g, st);
+  }
   AdmmStore a;
   a.z1 = z1;
   a.u1 = u1;
@@ -686,6 +698,7 @@ void shearlet_admm_shrink(Shearlet& sp, const float* f, int64_t batch, float* z1
 
 void shearlet_admm_synth(Shearlet& sp, const float* z1, const float* u1, int64_t batch, float* image,
                          cudaStream_t st) {
+  if (!shearlet_pow2(sp.height)) return shearlet_backward_generic(sp, RK_F32, z1, u1, batch, image, st);
   backward_impl<float, float>(sp, z1, u1, batch, image, st);
 }
 

@@ -55,9 +55,8 @@ void build_shearlet(Shearlet& sp, int64_t height, int64_t width, const std::vect
     throw ValidationError("shearlet plan needs between 1 and 8 scales, got " + std::to_string(alphas.size()));
   for (double a : alphas)
     if (!(a >= 0.0 && a <= 1.0)) throw ValidationError("shearlet alpha " + std::to_string(a) + " is outside [0, 1]");
-  if (sp.device >= 0 && ((height & (height - 1)) != 0 || height > 8192))
-    throw ValidationError("the device shearlet transform needs a power-of-two grid <= 8192, got " +
-                          std::to_string(height));
+  if (sp.device >= 0 && height > 8192)
+    throw ValidationError("the device shearlet transform supports grids up to 8192, got " + std::to_string(height));
   const int64_t h = height, w = width, J = int64_t(alphas.size());
   sp.height = h;
   sp.width = w;

@@ -138,8 +138,30 @@ def test_shape_validation(rk, cuda):
     for bad in ((1, 58, 32, 32), (1, 59, 16, 16)):
         with pytest.raises(rk.ValidationError):
             rk.backward(p, torch.zeros(*bad, device=cuda))
-    with pytest.raises(rk.ValidationError, match="power-of-two"):
-        rk.make_plan(48, 48, [0.5])
+    with pytest.raises(rk.ValidationError, match="square"):
+        rk.make_plan(48, 40, [0.5])
+
+
+@pytest.mark.parametrize("n,alphas,batch", [(2, [0.5], 2), (3, [0.5], 1), (10, [0.5, 0.5], 3), (24, [0.0, 1.0], 2),
+                                            (48, A5[:3], 2), (100, A5, 1)])
+def test_non_power_of_two_grids_match_reference(rk, ref, cuda, n, alphas, batch):
+    """Any square grid >= 2, as the reference's FFTW plans (shearlet.cpp:68-80): grids that
+    are not a power of two run shearlet_generic.cu's DFT-matrix transforms; fp32 and fp64
+    against the reference compiled in place, and the round trip."""
+    rng = np.random.default_rng(n)
+    p = rk.make_plan(n, n, alphas)
+    for dt, tol in ((np.float32, 1e-5), (np.float64, 1e-12)):
+        x = rng.standard_normal((batch, n, n)).astype(dt)
+        c = host(rk.forward(p, dev(x, cuda)))
+        cr = ref.shearlet_forward(x, alphas)
+        assert c.shape == cr.shape and c.dtype == dt
+        assert rel_l2(c, cr) <= tol, dt
+        b = host(rk.backward(p, dev(cr, cuda)))
+        assert rel_l2(b, ref.shearlet_backward(cr, alphas)) <= tol, dt
+        assert rel_l2(host(rk.backward(p, dev(c, cuda))), x) <= (1e-5 if dt == np.float32 else 1e-12)
+    xh = rng.standard_normal((batch, n, n)).astype(np.float16)
+    ch = host(rk.forward(p, dev(xh, cuda)))
+    assert rel_l2(ch.astype(np.float64), ref.shearlet_forward(xh, alphas).astype(np.float64)) <= 1e-3
 
 
 def test_host_arrays_round_trip_through_device(rk, ref, cuda):

@@ -62,7 +62,7 @@ for c in range(n_cases):
 
 # shearlets on random power-of-two grids and scale lists
 for c in range(max(4, n_cases // 4)):
-    n = int(rs.choice([2, 4, 8, 16, 32, 64, 128, 256]))
+    n = int(rs.choice([2, 3, 4, 8, 10, 16, 24, 32, 50, 64, 100, 128, 256]))  # any square grid
     alphas = list(np.round(rs.uniform(0, 1, int(rs.integers(1, 6))), 3))
     B = int(rs.integers(1, 4))
     dt = np.float32 if rs.random() < 0.7 else np.float64
@@ -78,7 +78,7 @@ for c in range(max(4, n_cases // 4)):
 
 # a few short ADMMs (512-angle sinograms are the paper's; small here)
 for c in range(max(2, n_cases // 10)):
-    s = int(rs.choice([32, 64]))
+    s = int(rs.choice([24, 32, 40, 64]))
     na = int(rs.integers(16, 48))
     ang = list(np.linspace(-np.pi / 4, np.pi / 4, na))
     g = rk.make_parallel(s, ang)
