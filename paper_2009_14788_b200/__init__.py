@@ -13,7 +13,7 @@ from .errors import (CudaError, DivergenceError, HalfOverflowError, NotPositiveD
                      ValidationError)
 from .geometry import (FanbeamGeometry, Geometry, ParallelGeometry, angles_linspace, geometry_det_count,
                        geometry_image_size, geometry_n_angles, make_fanbeam, make_parallel)
-from .projector import ProjectorOptions, backprojection, get_plan
+from .projector import ProjectorOptions, backprojection, get_plan, materialize_matrix
 from .projector import forward as _projector_forward
 from .sino_filter import FilterKind, FilterSpec, fbp, filter_kind_from_name, filter_kind_name, filter_sinogram, make_filter
 from .linop import (LinearOperator, adjoint_check, compose, gradient_check, identity_operator, projector_operator)
@@ -38,7 +38,7 @@ __all__ = [
     "CudaError", "DivergenceError", "HalfOverflowError", "NotPositiveDefiniteError", "NumericalError",
     "ValidationError", "FanbeamGeometry", "Geometry", "ParallelGeometry", "angles_linspace", "geometry_det_count",
     "geometry_image_size", "geometry_n_angles", "make_fanbeam", "make_parallel", "ProjectorOptions",
-    "backprojection", "forward", "get_plan", "FilterKind", "FilterSpec", "fbp", "filter_kind_from_name",
+    "backprojection", "forward", "get_plan", "materialize_matrix", "FilterKind", "FilterSpec", "fbp", "filter_kind_from_name",
     "filter_kind_name", "filter_sinogram", "make_filter", "LinearOperator", "adjoint_check", "compose",
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
     "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",

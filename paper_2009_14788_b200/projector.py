@@ -15,6 +15,8 @@ import threading
 from collections import OrderedDict
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _arrays as A
 from . import _lib
 from .errors import ValidationError
@@ -144,3 +146,26 @@ def backprojection(g: Geometry, sino, opts: ProjectorOptions | None = None):
     else:
         _lib.check(_lib.lib.rk_backproject_host(plan.handle, dt, A.ptr(sino), sino.shape[0], A.ptr(out)))
     return out
+
+
+def materialize_matrix(g: Geometry, opts: ProjectorOptions | None = None):
+    """projector.hpp:34 / projector.cpp:276-294: the dense (n_angles * det_count) x s^2
+    system matrix as a float64 numpy array, column c = forward of the unit image c (the
+    reference refuses image_size > 64).  The columns are projected in batches through
+    the host-buffer path (fp64 storage, fp32 compute like every projector call here)."""
+    _check_geometry(g)
+    s = int(g.image_size)
+    if s > 64:
+        raise ValidationError(f"materialize_matrix refuses image_size {s} (> 64); the dense matrix would be too large")
+    step = float((opts or ProjectorOptions()).step)
+    if not (step > 0.0):  # projector.cpp:31-33
+        raise ValidationError("projector step must be positive")
+    rows, cols = g.n_angles * g.det_count, s * s
+    mat = np.empty((rows, cols), np.float64)
+    per = max(1, min(cols, (256 << 20) // max(1, 8 * (rows + cols))))  # columns per batch, <= 256 MB
+    for c0 in range(0, cols, per):
+        n = min(per, cols - c0)
+        units = np.zeros((n, cols), np.float64)
+        units[np.arange(n), c0 + np.arange(n)] = 1.0
+        mat[:, c0:c0 + n] = np.asarray(forward(g, units.reshape(n, s, s), opts)).reshape(n, rows).T
+    return mat

@@ -440,3 +440,23 @@ def test_coarse_detector_and_narrow_detector_parity(rk, oracle, cuda, name, mk, 
     y = rs.standard_normal((B, g.n_angles, g.det_count)).astype(np.float32)
     b = host(rk.backprojection(g, dev(y, cuda)))
     assert rel_l2(b, oracle.backprojection(ogeom(g), y)) <= TOL32
+
+
+def test_materialize_matrix(rk, oracle, cuda):
+    """projector.cpp:276-294 / test_projector.cpp:57-110: the 2x2 single-angle matrix exactly,
+    the dense matrix against the reference's forward columns and A x against forward(x), and
+    the > 64 refusal."""
+    A = rk.materialize_matrix(rk.make_parallel(2, [0.0]))
+    assert A.shape == (2, 4) and A.dtype == np.float64
+    assert np.array_equal(A, np.array([[1.0, 0.0, 1.0, 0.0], [0.0, 1.0, 0.0, 1.0]]))
+    for g in (par(rk, 32, 45), fan(rk, 16, 24, 32.0)):
+        M = rk.materialize_matrix(g)
+        s = g.image_size
+        units = np.eye(s * s).reshape(s * s, s, s)
+        ref = oracle.forward(ogeom(g), units).reshape(s * s, -1).T
+        assert rel_l2(M, ref) <= TOL32
+        x = np.random.default_rng(7).uniform(-1.0, 1.0, (1, s, s))
+        fx = np.asarray(rk.forward(g, x)).reshape(-1)
+        assert rel_l2(M @ x.reshape(-1), fx) <= TOL32
+    with pytest.raises(rk.ValidationError, match="refuses image_size 65"):
+        rk.materialize_matrix(rk.make_parallel(65, [0.0]))
