@@ -446,9 +446,17 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
 // dq = lx c - ly s and dd = -lx s - ly c both numerator and denominator are
 // affine in the tile offsets (lx, ly): num = A lx + B ly, den = den00 + C lx +
 // D ly (A, B from fp64), and every lx term is shared by a thread's pixels.
-enum { kBpParallel = 0, kBpFan32 = 1, kBpFan64 = 2 };
+// kBpParHP (parallel beam, wide windows: fine detector spacing): kf reaches
+// the window width (hundreds to thousands of cells), where one fp32 ulp is a
+// visible weight error, so kf is carried as an exact "hi" part (multiples of
+// 2^-10 below 2^14: every partial sum is exact in fp32) plus a small "lo"
+// correction; floor and fraction come from hi, lo is added to the fraction.
+enum { kBpParallel = 0, kBpFan32 = 1, kBpFan64 = 2, kBpParHP = 3 };
 struct ParConst {
   float base, cx, cy, pad;
+};
+struct ParHPConst {
+  float base_hi, cx_hi, cy_hi, base_lo, cx_lo, cy_lo, pad0, pad1;
 };
 struct Fan32Const {
   float base, a, b, den00, c, d, pad0, pad1;
@@ -468,6 +476,10 @@ template <>
 struct BpConst<kBpFan64> {
   using type = FanConst;
 };
+template <>
+struct BpConst<kBpParHP> {
+  using type = ParHPConst;
+};
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -476,6 +488,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 constexpr int kTile = 32;
+constexpr int kBpHPWindow = 128;  // staged cells above which kf leaves the fp32-exact range (kBpParHP / kBpFan64)
 constexpr int kMaxBpChunk = 32;  // angles per staging pass (one constants record per thread of the first warp)
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   // takes a 4 x 2 block (a warp an 8 x 4 block; block w * RPT + r of the
   // tile's 32), which keeps its cells within one bank period.
   auto pixel_of = [&](int t, int r, int& pr, int& pc) {
-    if constexpr (KIND == kBpParallel) {
+    if constexpr (KIND == kBpParallel || KIND == kBpParHP) {
       pr = (t >> 5) + r * (kTile / RPT);
       pc = t & 31;
     } else {
@@ -579,17 +592,30 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
       const double x1 = x0 + double(min(kTile, s - j0) - 1), y1 = y0 - double(min(kTile, s - i0) - 1);
       double lo;
       Const k;
-      if constexpr (KIND == kBpParallel) {
+      if constexpr (KIND == kBpParallel || KIND == kBpParHP) {
         const double k00 = (x0 * c + y0 * sn) / spacing + off;
         const double k10 = (x1 * c + y0 * sn) / spacing + off;
         const double k01 = (x0 * c + y1 * sn) / spacing + off;
         const double k11 = (x1 * c + y1 * sn) / spacing + off;
         lo = fmin(fmin(k00, k10), fmin(k01, k11));
         const int ws = max(int(floor(lo)) - 1, -2);  // clipped like the host window (plan.cpp)
-        k.base = float(k00 - double(ws));
-        k.cx = float(c / spacing);
-        k.cy = float(-sn / spacing);
-        k.pad = 0.f;
+        if constexpr (KIND == kBpParallel) {
+          k.base = float(k00 - double(ws));
+          k.cx = float(c / spacing);
+          k.cy = float(-sn / spacing);
+          k.pad = 0.f;
+        } else {
+          constexpr double q = 1.0 / 1024.0;  // hi parts: multiples of 2^-10
+          const double base = k00 - double(ws), cx = c / spacing, cy = -sn / spacing;
+          const double bh = rint(base / q) * q, xh = rint(cx / q) * q, yh = rint(cy / q) * q;
+          k.base_hi = float(bh);
+          k.cx_hi = float(xh);
+          k.cy_hi = float(yh);
+          k.base_lo = float(base - bh);
+          k.cx_lo = float(cx - xh);
+          k.cy_lo = float(cy - yh);
+          k.pad0 = k.pad1 = 0.f;
+        }
         ws_s[tid] = ws;
       } else {
         auto kfan = [&](double x, double y) {
@@ -662,6 +688,10 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
       // fan (fp32 map): the row terms (a thread's pixels share one row)
       float col0 = 0.f, nrow = 0.f, drow = 0.f;
       if constexpr (KIND == kBpParallel) col0 = fmaf(float(tx), k.cx, k.base);
+      if constexpr (KIND == kBpParHP) {
+        col0 = fmaf(float(tx), k.cx_hi, k.base_hi);  // exact
+        nrow = fmaf(float(tx), k.cx_lo, k.base_lo);  // the small correction
+      }
       if constexpr (KIND == kBpFan32) {
         int pr0, pc0;
         pixel_of(tid, 0, pr0, pc0);
@@ -679,23 +709,40 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
             drow = fmaf(k.d, ly, k.den00);
           }
         }
-        float kf;
+        float fk, wt;
         if constexpr (KIND == kBpParallel) {
-          kf = fmaf(ly, k.cy, col0);
+          const float kf = fmaf(ly, k.cy, col0);
+          fk = floorf(kf);
+          wt = kf - fk;
+        } else if constexpr (KIND == kBpParHP) {
+          const float hi = fmaf(ly, k.cy_hi, col0);  // exact (multiples of 2^-10 below 2^14)
+          const float lo = fmaf(ly, k.cy_lo, nrow);
+          fk = floorf(hi);
+          wt = (hi - fk) + lo;  // hi - fk exact
+          if (wt >= 1.f) {
+            fk += 1.f;
+            wt -= 1.f;
+          } else if (wt < 0.f) {
+            fk -= 1.f;
+            wt += 1.f;
+          }
         } else if constexpr (KIND == kBpFan32) {
           const float num = fmaf(k.a, lx, nrow);  // (qx - qx00) K - u00 (den - den00)
           const float den = fmaf(k.c, lx, drow);  // qy + D_so
-          kf = fmaf(num, rcp_approx(den), k.base);
+          const float kf = fmaf(num, rcp_approx(den), k.base);
+          fk = floorf(kf);
+          wt = kf - fk;
         } else {
           const double dlx = double(lx), dly = double(ly);
           const double qx = fma(dlx, k.c, fma(-dly, k.s, k.qx00));
           const double den = fma(-dlx, k.s, fma(-dly, k.c, k.den00));
           double r = double(rcp_approx(float(den)));
           r = fma(r, fma(-den, r, 1.0), r);  // one Newton step: ~1e-14 relative
-          kf = float(fma(qx * kmag, r, k.offw));
+          const double kd = fma(qx * kmag, r, k.offw);
+          const double fd = floor(kd);  // floor and fraction in fp64: kf can be thousands of cells
+          fk = float(fd);
+          wt = float(kd - fd);
         }
-        const float fk = floorf(kf);
-        const float wt = kf - fk;
         const int c0 = min(max(int(fk), 0), window - 2);
         const float wl = 1.f - wt;
         if constexpr (LANE) {
@@ -889,31 +936,35 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
   dim3 grid(tiles, tiles, unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
   const bool lane = single_lane(batch);
   const bool wide = !lane && !h8 && wide_bp(groups_of(batch));
-  const int kind = p.g.kind != RK_FANBEAM ? kBpParallel : (p.bp_fan_fp64 ? kBpFan64 : kBpFan32);
+  // wide windows (fine detectors): kf spans hundreds of cells, so parallel beam carries it in
+  // two parts and fan beam uses the fp64 map (r2 extreme-geometry sweep, tools/stress_extreme.py)
+  const bool fan = p.g.kind == RK_FANBEAM;
+  const int kind = !fan ? (p.bp_window > kBpHPWindow ? kBpParHP : kBpParallel)
+                        : (p.bp_fan_fp64 || p.bp_window > 2 * kBpHPWindow ? kBpFan64 : kBpFan32);
   const bool narrow = !lane && !h8 && !wide && kind != kBpFan64 && narrow_bp();
   dim3 block(kTile, kTile / (narrow ? 8 : (lane || h8 || wide) ? 2 : kRowsPerThread));
-  const size_t rec = kind == kBpParallel ? sizeof(ParConst) : kind == kBpFan32 ? sizeof(Fan32Const) : sizeof(FanConst);
+  const size_t rec = kind == kBpParallel ? sizeof(ParConst)
+                     : kind == kBpParHP  ? sizeof(ParHPConst)
+                     : kind == kBpFan32  ? sizeof(Fan32Const)
+                                         : sizeof(FanConst);
   const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
-    auto kern = lane ? (kind == kBpParallel ? backproject_kernel<kBpParallel, T, true>
-                        : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, true>
-                                            : backproject_kernel<kBpFan64, T, true>)
-                     : (kind == kBpParallel ? backproject_kernel<kBpParallel, T, false>
-                        : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false>
-                                            : backproject_kernel<kBpFan64, T, false>);
-    if (narrow)
-      kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, false, false, true>
-                                 : backproject_kernel<kBpFan32, T, false, false, false, true>;
-    if (wide)
-      kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, false, true>
-             : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, false, true>
-                                 : backproject_kernel<kBpFan64, T, false, false, true>;
-    if constexpr (std::is_same<T, __half>::value)
-      if (h8)
-        kern = kind == kBpParallel ? backproject_kernel<kBpParallel, T, false, true>
-               : kind == kBpFan32  ? backproject_kernel<kBpFan32, T, false, true>
-                                   : backproject_kernel<kBpFan64, T, false, true>;
+    // the kernel variant for one kind: single-lane (batch 1), half8, WIDE (one group), NARROW or 256 x 4
+    auto pick = [&](auto kind_tag) {
+      constexpr int K = decltype(kind_tag)::value;
+      auto kern = lane ? backproject_kernel<K, T, true> : backproject_kernel<K, T, false>;
+      if constexpr (K != kBpFan64)
+        if (narrow) kern = backproject_kernel<K, T, false, false, false, true>;
+      if (wide) kern = backproject_kernel<K, T, false, false, true>;
+      if constexpr (std::is_same<T, __half>::value)
+        if (h8) kern = backproject_kernel<K, T, false, true>;
+      return kern;
+    };
+    auto kern = kind == kBpParallel ? pick(std::integral_constant<int, kBpParallel>{})
+                : kind == kBpParHP  ? pick(std::integral_constant<int, kBpParHP>{})
+                : kind == kBpFan32  ? pick(std::integral_constant<int, kBpFan32>{})
+                                    : pick(std::integral_constant<int, kBpFan64>{});
     allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,

@@ -426,12 +426,18 @@ def test_backprojector_thread_shapes_equal_bitwise(rk, oracle, cuda, tmp_path):
     ("par-128-det10-sp14", lambda rk: par(rk, 128, 33, 10, 14.0)),
     ("par-160-det20-sp8", lambda rk: par(rk, 160, 50, 20, 8.0)),
     ("par-100-det35-one-angle", lambda rk: rk.make_parallel(100, [-2.8931329237874532], 35, 1.0)),
+    # fine detectors: backprojection windows of hundreds of cells (kBpParHP, fp64 fan map)
+    ("par-128-det1800-sp0.1", lambda rk: par(rk, 128, 30, 1800, 0.1)),
+    ("par-96-det4096-sp0.03", lambda rk: par(rk, 96, 12, 4096, 0.03)),
+    ("fan-128-det1200-sp0.25", lambda rk: fan(rk, 128, 24, 256.0, det_count=1200, det_spacing=0.25)),
 ])
 @pytest.mark.parametrize("B", [1, 5])
 def test_coarse_detector_and_narrow_detector_parity(rk, oracle, cuda, name, mk, B):
     """Detectors much coarser than the pixels (rays several pixels apart: the forward planner's
-    narrow-warp tiers) and detectors narrower than the image (the backprojection window must
-    cover every tile row, plan.cpp) — both found by tools/stress_parity.py in r2."""
+    narrow-warp tiers), detectors narrower than the image (the backprojection window must
+    cover every tile row, plan.cpp) and much finer ones (kf spans hundreds of cells: the
+    two-part parallel kernel, the fp64 fan map) — found by tools/stress_parity.py and
+    tools/stress_extreme.py in r2."""
     g = mk(rk)
     rs = np.random.default_rng(17)
     x = rs.uniform(0.0, 1.0, (B, g.image_size, g.image_size)).astype(np.float32)

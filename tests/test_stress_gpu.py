@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("tool,args", [("stress_parity.py", ["250", "31", "300"]),
                                        ("stress_parity.py", ["250", "32", "520"]),
-                                       ("stress_solvers.py", ["16", "33"])])
+                                       ("stress_solvers.py", ["16", "33"]),
+                                       ("stress_extreme.py", ["8", "34"])])
 def test_randomised_sweep(tool, args):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", tool), *args], capture_output=True, text=True,
                        timeout=900, cwd=ROOT)
