@@ -14,12 +14,16 @@
 // the first forward, last forward and last inverse passes (filter_kernel).
 #include <cuda_fp16.h>
 
+#include <cooperative_groups.h>
+
 #include <type_traits>
 
 #include "fft_smem.cuh"
 #include "rk_internal.hpp"
 
 namespace rk {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -54,11 +58,12 @@ constexpr int kFilterThreads = 256;
 // ZERO_TOP: inputs i >= n/2 are known zero (the zero-padded half of the row):
 // the group's upper elements are not loaded and the first butterfly layer
 // (partner bit R-1 of a DIF pass at the widest stride) reduces to u, u W.
-template <int R, bool DIF, bool CONJ, bool ZERO_TOP, class Load, class Store>
+// NSEQ: complex sequences per CTA (2; the split kernel below runs 1).
+template <int R, bool DIF, bool CONJ, bool ZERO_TOP, class Load, class Store, int NSEQ = 2>
 __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, Load load, Store store) {
   const int gl = logn - R;
 #pragma unroll 4
-  for (int t = threadIdx.x; t < (2 << gl); t += kFilterThreads) {
+  for (int t = threadIdx.x; t < (NSEQ << gl); t += kFilterThreads) {
     const int seq = t >> gl, g = t & ((1 << gl) - 1);
     const int lo = g & ((1 << lh) - 1), hi = g >> lh;
     const int i0 = lo + (hi << (lh + R));
@@ -214,6 +219,99 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
   if (logP - lq == 1) filter_pass<1, false, true, false>(logP, lq, tws, sm_load, out_store);
 }
 
+// Transforms of P = 2^14 and 2^15 points (det_count 4097 .. 16384) no longer
+// fit one CTA's shared memory, so a two-CTA cluster splits each sequence into
+// its even and odd frequencies.  The row is zero beyond det_count <= P/2, so
+// the first DIF layer needs no exchange: y_0[i] = x[i] and y_1[i] = x[i] W_P^i
+// (i < P/2) are the two half-size inputs, whose P/2-point DIF transforms are
+// the even (rank 0) and odd (rank 1) frequency bins.  Each CTA applies the
+// response to its bins (frequency 2 brev(q) + rank) and runs the P/2-point
+// inverse DIT; the last inverse layer would combine the halves,
+//   out[i] = a[i] + conj(W_P^i) b[i]   (only i < det_count <= P/2 is kept),
+// so after a cluster barrier each CTA reads the other's half through
+// distributed shared memory for its share of the outputs.  One complex
+// sequence (two rows) per cluster; P/2 complex in each CTA (64 / 128 KB).
+template <class TIn, class TOut, int PACKED, int LOGH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFilterThreads)
+    filter_split_kernel(const TIn* __restrict__ in, int64_t batch, int na, int nd, const float* __restrict__ resp,
+                        const float2* __restrict__ tw, float scale, TOut* __restrict__ out,
+                        float4* __restrict__ packed) {
+  constexpr int H = 1 << LOGH, P = 2 * H, logH = LOGH;
+  extern __shared__ float2 fsm[];
+  float2* za = fsm;  // this CTA's half, swizzled slots (fft_swz)
+  const unsigned rank = blockIdx.x & 1u;  // cluster rank: 0 even, 1 odd frequencies
+  const int a = int(blockIdx.x >> 1);
+  const int64_t g = blockIdx.y;
+  const int seq = int(blockIdx.z);  // rows 2 seq (re) and 2 seq + 1 (im) of packed group g
+  const int64_t b_re = g * kPack + 2 * seq, b_im = b_re + 1;
+  const bool vre = b_re < batch, vim = b_im < batch;
+  const TIn* pre = in + (vre ? (b_re * na + a) * int64_t(nd) : 0);
+  const TIn* pim = in + (vim ? (b_im * na + a) * int64_t(nd) : 0);
+  const float2* wP = tw + (H - 1);  // stage logP - 1: W_P^k, k < P/2
+  auto sm_load = [&](int, int i, int) { return za[fft_swz(i)]; };
+  auto sm_store = [&](int, int i, int, float2 v) { za[fft_swz(i)] = v; };
+  auto gl_load = [&](int, int i, int) {  // y_rank[i]
+    float re = 0.f, im = 0.f;
+    if (i < nd) {
+      if (vre) re = ld_f32(pre + i);
+      if (vim) im = ld_f32(pim + i);
+    }
+    float2 v = make_float2(re, im);
+    if (rank) v = fft_cmul(v, __ldg(wP + i));
+    return v;
+  };
+  constexpr int shift = 32 - logH;
+  auto mul_store = [&](int, int i, int, float2 v) {
+    const int f = 2 * int(__brev(unsigned(i)) >> shift) + int(rank);
+    const float h = __ldg(resp + (f <= P / 2 ? f : P - f));
+    za[fft_swz(i)] = make_float2(v.x * h, v.y * h);
+  };
+  // ---- forward DIF of the half (natural -> bit-reversed)
+  constexpr int r0 = logH % 3 == 0 ? 3 : logH % 3;
+  int lh = logH - r0;
+  filter_pass<r0, true, false, false, decltype(gl_load), decltype(sm_store), 1>(logH, lh, tw, gl_load, sm_store);
+#pragma unroll
+  while (lh >= 3) {
+    lh -= 3;
+    if (lh == 0)
+      filter_pass<3, true, false, false, decltype(sm_load), decltype(mul_store), 1>(logH, lh, tw, sm_load, mul_store);
+    else
+      filter_pass<3, true, false, false, decltype(sm_load), decltype(sm_store), 1>(logH, lh, tw, sm_load, sm_store);
+  }
+  // ---- inverse DIT of the half (bit-reversed -> natural), into shared memory
+  int lq = 0;
+#pragma unroll
+  for (; lq + 3 <= logH; lq += 3)
+    filter_pass<3, false, true, false, decltype(sm_load), decltype(sm_store), 1>(logH, lq, tw, sm_load, sm_store);
+  if (logH - lq == 2) filter_pass<2, false, true, false, decltype(sm_load), decltype(sm_store), 1>(logH, lq, tw, sm_load, sm_store);
+  if (logH - lq == 1) filter_pass<1, false, true, false, decltype(sm_load), decltype(sm_store), 1>(logH, lq, tw, sm_load, sm_store);
+  // ---- combine across the cluster: out[i] = a[i] + conj(W_P^i) b[i], crop, x 1/P, x pi/(2 na)
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  const float2* za0 = cluster.map_shared_rank(za, 0);
+  const float2* za1 = cluster.map_shared_rank(za, 1);
+  const float inv = 1.0f / float(P);
+  const int half_nd = (nd + 1) / 2;
+  for (int i = int(rank) * half_nd + threadIdx.x; i < min(nd, (int(rank) + 1) * half_nd); i += kFilterThreads) {
+    const float2 av = za0[fft_swz(i)], bv = za1[fft_swz(i)];
+    const float2 v = make_float2(av.x, av.y);
+    const float2 wb = fft_cmul_conj(bv, __ldg(wP + i));
+    const float v0 = ((v.x + wb.x) * inv) * scale, v1 = ((v.y + wb.y) * inv) * scale;
+    if (PACKED == 2) {
+      const unsigned bits = unsigned(__half_as_ushort(__float2half_rn(v0))) |
+                            (unsigned(__half_as_ushort(__float2half_rn(v1))) << 16);
+      reinterpret_cast<unsigned*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + i) * 4 + (g & 1) * 2 + seq] = bits;
+    } else if (PACKED == 1) {
+      reinterpret_cast<float2*>(packed)[((g * na + a) * int64_t(nd) + i) * 2 + seq] =
+          make_float2(float(st_cast<TOut>(v0)), float(st_cast<TOut>(v1)));
+    } else {
+      if (vre) out[(b_re * na + a) * int64_t(nd) + i] = st_cast<TOut>(v0);
+      if (vim) out[(b_im * na + a) * int64_t(nd) + i] = st_cast<TOut>(v1);
+    }
+  }
+  cluster.sync();  // the other CTA may still read this one's half
+}
+
 template <class F>
 void dispatch(int dtype, F&& f) {
   switch (dtype) {
@@ -234,6 +332,27 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   const size_t smem = size_t(2) * P * sizeof(float2);  // two sequences
   const float scale = float(M_PI / (2.0 * double(n_angles)));  // sino_filter.cpp:108
   dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
+  if (logP >= 14) {  // 2^14, 2^15 (det_count 4097 .. 16384): the two-CTA cluster kernel
+    const size_t hsmem = size_t(P / 2) * sizeof(float2);
+    dim3 sgrid(unsigned(2 * n_angles), unsigned(groups_of(batch)), 2u);
+    dispatch(dtype, [&](auto tag) {
+      using T = decltype(tag);
+      auto pick = [&](auto packed_tag) {
+        constexpr int PK = decltype(packed_tag)::value;
+        return logP == 14 ? filter_split_kernel<T, T, PK, 13> : filter_split_kernel<T, T, PK, 14>;
+      };
+      auto kern = packed_out ? pick(std::integral_constant<int, 1>{}) : pick(std::integral_constant<int, 0>{});
+      if constexpr (std::is_same<T, __half>::value)
+        if (packed_out && use_h8(dtype, batch)) kern = pick(std::integral_constant<int, 2>{});
+      allow_dynamic_smem(reinterpret_cast<const void*>(kern), hsmem);
+      KernelTimer timer(RK_KERNEL_FILTER, st);
+      kern<<<sgrid, kFilterThreads, hsmem, st>>>(static_cast<const T*>(in), batch, int(n_angles), int(f.det_count),
+                                                 f.d_response.as<float>(), f.d_twiddle_stage.as<float2>(), scale,
+                                                 static_cast<T*>(out), packed_out);
+    });
+    RK_CUDA(cudaGetLastError());
+    return;
+  }
   dispatch(dtype, [&](auto tag) {
     using T = decltype(tag);
     // compile-time sizes for P = 2^9 .. 2^13 (det_count 129 .. 4096), run-time size otherwise

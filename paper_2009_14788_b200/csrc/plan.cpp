@@ -379,9 +379,9 @@ void build_filter(Filter& f, int kind, int64_t det_count) {
   int64_t n = 1;
   while (n < 2 * det_count) n <<= 1;
   n = std::max<int64_t>(n, 2);
-  if (n > 8192)
+  if (n > 32768)
     throw ValidationError("det_count " + std::to_string(det_count) + " pads to " + std::to_string(n) +
-                          " > 8192, beyond the shared-memory FFT of the filter kernel");
+                          " > 32768, beyond the two-CTA shared-memory FFT of the filter kernel");
   f.kind = kind;
   f.det_count = det_count;
   f.padded = n;

@@ -251,3 +251,25 @@ def test_config5_landweber_parity(rk, oracle, cuda):
         out = host(rk.landweber(rk.projector_operator(g), dev(y, cuda), torch.zeros(2, 512, 512, device=cuda),
                                 ref_alpha, 3))
         assert rel_l2(out, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("nd", [4097, 9000, 16384])
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-5), (np.float16, 1e-3)])
+def test_filter_large_detectors_cluster_kernel(rk, oracle, cuda, nd, dtype, tol):
+    """det_count 4097 .. 16384 pads to 2^14 / 2^15 points: the two-CTA cluster filter kernel
+    (even / odd frequency halves, combined through distributed shared memory); the reference
+    filters any size (sino_filter.cpp:98-124).  Filter and FBP against the reference."""
+    rs = np.random.default_rng(nd)
+    scale = 0.01 if dtype == np.float16 else 1.0
+    y = (rs.standard_normal((5, 3, nd)) * scale).astype(dtype)
+    for kind in ("ram-lak", "shepp-logan"):
+        f = host(rk.filter_sinogram(dev(y, cuda), rk.make_filter(rk.filter_kind_from_name(kind), nd)))
+        assert rel_l2(f.astype(np.float64), oracle.filter_sinogram(y, kind).astype(np.float64)) <= tol, kind
+    g = rk.make_parallel(48, rk.angles_linspace(0.0, np.pi, 3), nd, 0.02)
+    fb = host(rk.fbp(g, dev(y, cuda)))
+    assert rel_l2(fb.astype(np.float64), oracle.fbp(ogeom(g), y).astype(np.float64)) <= tol
+
+
+def test_filter_size_limit(rk):
+    with pytest.raises(rk.ValidationError, match="pads to 65536 > 32768"):
+        rk.make_filter(rk.FilterKind.RamLak, 16385)
