@@ -141,7 +141,9 @@ int rk_backproject(rk_plan* plan, int dtype, const void* d_sino, int64_t batch, 
 int rk_filter_kind_from_name(const char* name, int* kind);
 const char* rk_filter_kind_name(int kind);
 /* Ramp response of make_filter (sino_filter.cpp:64-92), uploaded to `device`
- * (device -1: host-only, for inspecting the response without a GPU). */
+ * (device -1: host-only, for inspecting the response without a GPU).
+ * det_count 2 .. 16384 (padded transforms up to 2^15 points; above 2^13 the
+ * filter runs on two-CTA clusters). */
 int rk_filter_create(int kind, int64_t det_count, int device, rk_filter** filter);
 int rk_filter_destroy(rk_filter* filter);
 /* Host copy of the response: padded size, padded/2+1 double and float bins
@@ -181,8 +183,9 @@ int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int6
 /* ------------------------------------------------------------- shearlets + ADMM */
 typedef struct rk_shearlet rk_shearlet;
 /* make_plan (shearlet.hpp:37): cone-adapted alpha-shearlet Fourier multipliers,
- * Parseval-normalised; power-of-two square grids on the device.  device -1:
- * host-only (multipliers for inspection). */
+ * Parseval-normalised; any square grid >= 2 (<= 8192) on the device: radix-2
+ * shared-memory FFTs for powers of two, DFT-matrix transforms otherwise.
+ * device -1: host-only (multipliers for inspection). */
 int rk_shearlet_create(int64_t height, int64_t width, const double* alphas, int n_scales, int device,
                        rk_shearlet** plan);
 /* make_plan_cached (shearlet.hpp:43, shearlet.cpp:201-249): a plan over stored
