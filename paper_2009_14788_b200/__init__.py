@@ -23,6 +23,7 @@ from . import shearlet
 from .shearlet import ShearletPlan, backward, make_plan, make_plan_cached, shearlet_operator
 from .admm import AdmmParams, AdmmState, admm_objective, admm_reconstruct, default_weights, shrink
 from .npy import read_array, write_array
+from .png_io import png_export
 
 
 def forward(plan_or_geometry, x, *args, **kwargs):
@@ -43,5 +44,5 @@ __all__ = [
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
     "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",
     "AdmmParams", "AdmmState", "admm_objective", "admm_reconstruct", "default_weights", "shrink",
-    "read_array", "write_array",
+    "read_array", "write_array", "png_export",
 ]

@@ -1,7 +1,7 @@
 """Command-line front end for the hot path — the subcommands of the reference
 CLI that reach it (``proj/tools/cli.cpp``): ``project``, ``backproject``,
 ``filter``, ``fbp``, ``solve``, ``check-adjoint``, ``bench``, ``phantom``,
-``shearlet`` and ``admm``, with the same
+``shearlet``, ``admm`` and ``png-export``, with the same
 flags (angles in degrees, geometry defaults, ``--precision``), ``.npy`` files
 holding the natural rank (a batch dim is lifted/squeezed like
 ``lift_batch``/``squeeze_batch``, cli.cpp:109-129), the same ``--json``
@@ -201,6 +201,11 @@ def main(argv=None) -> int:
     p.add_argument("--progress", action="store_true", help="print the objective each outer iteration to stderr")
     p.add_argument("--cache-dir", default="")
     p.add_argument("--reference", default="")
+    p = sub.add_parser("png-export", help="render an array to a 16-bit grayscale PNG")
+    p.add_argument("--in", dest="inp", required=True, help="input image .npy")
+    p.add_argument("-o", "--out", required=True, help="output .png path")
+    p.add_argument("--lo", type=float, default=0.0, help="window low (maps to black)")
+    p.add_argument("--hi", type=float, default=1.0, help="window high (maps to white)")
     try:
         a = ap.parse_args(argv)
     except SystemExit as e:  # usage errors exit 1, --help / --version 0 (cli.cpp:711-716)
@@ -411,6 +416,9 @@ def _run(rk, a) -> int:
             print(f"admm: {a.outer} outer x {a.inner} inner iterations, objective {objective:.6e}, {secs:.3f} s")
             if a.reference:
                 print(f"mse vs reference: {rep['mse_vs_reference']:.6e}")
+        return 0
+    if a.cmd == "png-export":  # cli.cpp:690-708
+        rk.png_export(read_array(a.inp), a.out, a.lo, a.hi)
         return 0
     return 1
 
