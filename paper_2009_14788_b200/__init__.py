@@ -24,6 +24,7 @@ from .shearlet import ShearletPlan, backward, make_plan, make_plan_cached, shear
 from .admm import AdmmParams, AdmmState, admm_objective, admm_reconstruct, default_weights, shrink
 from .npy import read_array, write_array
 from .png_io import png_export
+from .threading import num_threads, set_num_threads
 
 
 def forward(plan_or_geometry, x, *args, **kwargs):
@@ -44,5 +45,5 @@ __all__ = [
     "gradient_check", "identity_operator", "projector_operator", "Rng", "cg", "cgne", "estimate_alpha", "landweber",
     "ShearletPlan", "backward", "make_plan", "make_plan_cached", "shearlet", "shearlet_operator",
     "AdmmParams", "AdmmState", "admm_objective", "admm_reconstruct", "default_weights", "shrink",
-    "read_array", "write_array", "png_export",
+    "read_array", "write_array", "png_export", "num_threads", "set_num_threads",
 ]

@@ -193,3 +193,23 @@ def test_plan_cache_is_lru(rk):
     finally:
         P._MAX_PLANS = old
         P._PLANS.clear()
+
+
+def test_set_num_threads_contract():
+    """threading.cpp:24-32: n >= 1 is kept, n < 1 is a ValidationError, the default is the
+    hardware count (here: the forward planner's host threads)."""
+    import os
+
+    import paper_2009_14788_b200 as rk
+
+    saved = os.environ.pop("RK_PLAN_THREADS", None)
+    try:
+        assert rk.num_threads() == (os.cpu_count() or 1)
+        rk.set_num_threads(3)
+        assert rk.num_threads() == 3
+        with pytest.raises(rk.ValidationError, match="thread count must be >= 1, got 0"):
+            rk.set_num_threads(0)
+    finally:
+        os.environ.pop("RK_PLAN_THREADS", None)
+        if saved is not None:
+            os.environ["RK_PLAN_THREADS"] = saved
