@@ -722,9 +722,16 @@ def measure_extras(rk, _lib, dev):
         rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=20, inner_cg_iterations=50))
         # median of three full calls: single runs on a shared box showed +25-50 % outliers
         # (tools/admm_var_probe.py: per-iteration device time is flat at 19.0 ms for batch 1)
-        runs = sorted(timed(lambda: rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=50,
-                                                                                    inner_cg_iterations=50)),
-                            runs=1) for _ in range(3))
+        runs = []
+        for _ in range(3):
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            a.record(st)
+            rk.admm_reconstruct(opa, plan, ya, rk.AdmmParams(outer_iterations=50, inner_cg_iterations=50))
+            e.record(st)
+            torch.cuda.synchronize(dev)
+            runs.append(a.elapsed_time(e))
+        runs.sort()
         ms = runs[1]
         out[f"next_admm512_limited100_na512_b{b}_fp32"] = {"metric": "ADMM seconds per image (50 outer x 50 inner)",
                                                            "value": ms * 1e-3 / b, "ms": ms,
