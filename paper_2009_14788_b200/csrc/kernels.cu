@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
   // this tile's staged cells per angle, and as many angles per pass as fit
   const int window = __ldg(tile_window + blockIdx.y * gridDim.x + blockIdx.x);
+  const int wc = window >> 1;  // middle cell (fp32 kinds measure kf from it)
   const int chunk = min(kMaxBpChunk, cells / window);
   Cell* win = smem;                                                    // chunk * window <= cells
   Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kMaxBpChunk records
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
         lo = fmin(fmin(k00, k10), fmin(k01, k11));
         const int ws = max(int(floor(lo)) - 1, -2);  // clipped like the host window (plan.cpp)
         if constexpr (KIND == kBpParallel) {
-          k.base = float(k00 - double(ws));
+          k.base = float(k00 - double(ws) - double(wc));  // relative to the window's middle cell
           k.cx = float(c / spacing);
           k.cy = float(-sn / spacing);
           k.pad = 0.f;
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
         const double den00 = -x0 * sn + y0 * c + source_distance;
         if constexpr (KIND == kBpFan32) {
           const double K = span / spacing, u00 = qx00 * K / den00;
-          k.base = float(k00 - double(ws));
+          k.base = float(k00 - double(ws) - double(wc));  // relative to the window's middle cell
           k.a = float(c * K + u00 * sn);
           k.b = float(u00 * c - sn * K);
           k.den00 = float(den00);
@@ -683,7 +684,9 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
     const double kmag = span / spacing;
     for (int q = 0; q < nac; ++q) {
       const Const k = cst[q];
-      const Cell* w = win + q * window;
+      // fp32 kinds: kf relative to the middle cell wc of the window (half the magnitude, half the
+      // fp32 rounding of kf); the pointer carries the offset back
+      const Cell* w = win + q * window + ((KIND == kBpParallel || KIND == kBpFan32) ? wc : 0);
       // parallel: the column term is shared by the thread's pixels (one column);
       // fan (fp32 map): the row terms (a thread's pixels share one row)
       float col0 = 0.f, nrow = 0.f, drow = 0.f;
@@ -729,7 +732,9 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
         } else if constexpr (KIND == kBpFan32) {
           const float num = fmaf(k.a, lx, nrow);  // (qx - qx00) K - u00 (den - den00)
           const float den = fmaf(k.c, lx, drow);  // qy + D_so
-          const float kf = fmaf(num, rcp_approx(den), k.base);
+          float r = rcp_approx(den);
+          r = fmaf(r, fmaf(-den, r, 1.f), r);  // one Newton step: the reciprocal to ~0.5 ulp
+          const float kf = fmaf(num, r, k.base);
           fk = floorf(kf);
           wt = kf - fk;
         } else {
@@ -743,7 +748,8 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
           fk = float(fd);
           wt = float(kd - fd);
         }
-        const int c0 = min(max(int(fk), 0), window - 2);
+        constexpr bool centred = KIND == kBpParallel || KIND == kBpFan32;
+        const int c0 = min(max(int(fk), centred ? -wc : 0), window - 2 - (centred ? wc : 0));
         const float wl = 1.f - wt;
         if constexpr (LANE) {
           const float s0 = w[c0], s1 = w[c0 + 1];

@@ -284,7 +284,7 @@ void build_plan(Plan& p) {
     const double mag = span / (g.det_spacing * (g.source_distance - rmax));
     static const double max_mag = [] {
       const char* e = std::getenv("RK_BP_FAN32_MAXMAG");
-      return e ? std::atof(e) : 4.0;
+      return e ? std::atof(e) : 3.5;
     }();
     p.bp_fan_fp64 = !(mag <= max_mag);
   }
