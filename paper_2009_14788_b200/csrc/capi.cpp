@@ -188,8 +188,12 @@ void run_host_pipeline(rk::HostPipeline& pipe, int device, std::mutex& mu, int64
   // chunk sizes: ramp up from one packed group and back down at the end, so
   // the copy-in before the first kernel and the copy-out after the last one
   // (the parts no kernel overlaps) are short
+  static const int64_t ramp_start = [] {  // RK_PIPE_RAMP_START: first / last chunk (images)
+    const char* e = std::getenv("RK_PIPE_RAMP_START");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(rk::kPack);
+  }();
   std::vector<int64_t> sizes, ramp;
-  for (int64_t c = rk::kPack; c < chunk; c *= 2) ramp.push_back(c);
+  for (int64_t c = ramp_start; c < chunk; c *= 2) ramp.push_back(c);
   int64_t ramp_total = 0;
   for (int64_t c : ramp) ramp_total += 2 * c;
   if (use_ramp && !ramp.empty() && batch >= ramp_total + chunk) {
