@@ -466,3 +466,15 @@ def test_materialize_matrix(rk, oracle, cuda):
         assert rel_l2(M @ x.reshape(-1), fx) <= TOL32
     with pytest.raises(rk.ValidationError, match="refuses image_size 65"):
         rk.materialize_matrix(rk.make_parallel(65, [0.0]))
+
+
+def test_very_large_batch(rk, oracle, cuda):
+    """2,049 images of 512^2 (2 GB in, 64-bit indexing, 513 packed groups): the first and last
+    elements match the reference and equal their single-image results bit for bit."""
+    import subprocess
+    import sys
+
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, __import__("os").path.join(root, "tools", "big_batch_probe.py"), "2049"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
