@@ -8,6 +8,7 @@
 //   3  as 2 with 16 FFMA2
 //   4  no conversion (taps reinterpreted as floats): 32 FFMA      (pipe floor)
 //   5  no conversion: 16 FFMA2
+//   6  split-weight mixed FMA: w = w_hi + w_lo (halves), 2 x fma.rn.f32.f16 per tap and image
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o pipe_rates pipe_rates.cu
 // Run:   ./pipe_rates   (prints ns per warp-iteration per SMSP for each variant)
 #include <cuda_fp16.h>
@@ -32,6 +33,11 @@ __device__ __forceinline__ float cvt_hi(unsigned w) {
 }
 // upper half of w as (value * 2^-112) in fp32 bits: sign to bit 31, the 15
 // magnitude bits to 27..13 (exact for normal and subnormal halves)
+__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float hi_scaled(unsigned w) {
   return __int_as_float(int(unsigned(int(w) >> 3)) & int(0x8FFFE000u));
 }
@@ -98,6 +104,30 @@ __global__ void __launch_bounds__(256, 4) kern(int iters, float* out) {
           a2[wd] = r;
         }
       }
+    } else if constexpr (V == 6) {
+      const float W[4] = {w1, w2, w3, w4};
+      unsigned short wh[4], wl[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const __half h = __float2half_rn(W[t]);
+        wh[t] = __half_as_ushort(h);
+        wl[t] = __half_as_ushort(__float2half_rn(W[t] - __half2float(h)));
+      }
+      const unsigned* UU[4] = {U1, U2, U3, U4};
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float a = acc[2 * wd + hh];
+#pragma unroll
+          for (int t = 3; t >= 0; --t) {
+            const unsigned short v = (unsigned short)(hh ? (UU[t][wd] >> 16) : (UU[t][wd] & 0xffffu));
+            a = fhfma(v, wl[t], a);
+            a = fhfma(v, wh[t], a);
+          }
+          acc[2 * wd + hh] = a;
+        }
+      }
     } else {
 #pragma unroll
       for (int wd = 0; wd < 4; ++wd) {
@@ -150,6 +180,7 @@ int main() {
   run<3>("cvt x16 + int-hi x16 + FFMA2 x16", out);
   run<4>("no cvt, FFMA x32", out);
   run<5>("no cvt, FFMA2 x16", out);
+  run<6>("split-weight FHFMA x64", out);
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
   return 0;
