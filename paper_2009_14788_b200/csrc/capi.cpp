@@ -247,6 +247,68 @@ void quiesce_plan(rk::Plan& p) {
 }
 }  // namespace
 
+struct rk_admm_state {
+  rk::Admm a;
+};
+
+namespace {
+// Finished ADMM states kept for the next call with the same plan, shearlet plan,
+// batch, dtype, penalties and inner iterations: their device buffers and the
+// captured outer-iteration graph are reused (admm_init re-zeroes the state), so a
+// repeated admm_reconstruct does not pay cudaMalloc / cudaFree / graph capture —
+// which made single calls vary by up to +50 % (destroy alone 2 .. 560 ms,
+// tools/admm_phase_probe.py).  Heap-allocated and never destroyed: the CUDA
+// context may be gone at static destruction.
+std::mutex g_admm_idle_mu;
+std::vector<rk_admm_state*>* g_admm_idle = new std::vector<rk_admm_state*>();
+constexpr size_t kAdmmIdleMax = 2;
+
+rk_admm_state* admm_take_idle(const rk::Plan* p, const rk::Shearlet* sh, int dtype, int64_t batch, float p0f,
+                              float p1f, int inner) {
+  std::lock_guard<std::mutex> lock(g_admm_idle_mu);
+  for (auto it = g_admm_idle->begin(); it != g_admm_idle->end(); ++it) {
+    const rk::Admm& a = (*it)->a;
+    if (a.plan == p && a.sh == sh && a.dtype == dtype && a.batch == batch && a.p0f == p0f && a.p1f == p1f &&
+        a.inner == inner) {
+      rk_admm_state* h = *it;
+      g_admm_idle->erase(it);
+      return h;
+    }
+  }
+  return nullptr;
+}
+
+void admm_release(rk_admm_state* h) {  // the state's work is complete (its caller synchronised)
+  rk_admm_state* evicted = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_admm_idle_mu);
+    g_admm_idle->push_back(h);
+    if (g_admm_idle->size() > kAdmmIdleMax) {
+      evicted = g_admm_idle->front();
+      g_admm_idle->erase(g_admm_idle->begin());
+    }
+  }
+  delete evicted;
+}
+
+// before a plan or shearlet plan goes away: drop the idle states that point at it
+void admm_purge(const rk::Plan* p, const rk::Shearlet* sh) {
+  std::vector<rk_admm_state*> drop;
+  {
+    std::lock_guard<std::mutex> lock(g_admm_idle_mu);
+    for (auto it = g_admm_idle->begin(); it != g_admm_idle->end();) {
+      if ((p && (*it)->a.plan == p) || (sh && (*it)->a.sh == sh)) {
+        drop.push_back(*it);
+        it = g_admm_idle->erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  for (auto* h : drop) delete h;
+}
+}  // namespace
+
 extern "C" {
 
 const char* rk_last_error(void) { return g_last_error.c_str(); }
@@ -294,6 +356,7 @@ int rk_plan_create(const rk_geometry* geometry, int device, rk_plan** plan) {
 int rk_plan_destroy(rk_plan* plan) {
   return guarded_named(__func__, [&] {
     if (!plan) return;
+    admm_purge(&plan->p, nullptr);  // idle ADMM states built on this plan
     {
       std::lock_guard<std::mutex> lock(plan->p.mu);  // no call is enqueueing on it
       quiesce_plan(plan->p);
@@ -598,6 +661,7 @@ int rk_shearlet_create_stored(int64_t height, int64_t width, const double* alpha
 int rk_shearlet_destroy(rk_shearlet* plan) {
   return guarded_named(__func__, [&] {
     if (!plan) return;
+    admm_purge(nullptr, &plan->s);  // idle ADMM states built on this shearlet plan
     if (plan->s.device >= 0) {
       if (cudaSetDevice(plan->s.device) == cudaSuccess) cudaDeviceSynchronize();
       cudaGetLastError();
@@ -676,9 +740,6 @@ std::vector<double> admm_thresholds(const rk::Shearlet& s, const double* weights
 }
 }  // namespace
 
-struct rk_admm_state {
-  rk::Admm a;
-};
 
 int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* d_sino, int64_t batch, double p0,
                    double p1, const double* weights, int inner_cg_iterations, void* stream, rk_admm_state** out) {
@@ -688,7 +749,9 @@ int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* 
     check_admm_args(plan, shearlet, dtype, batch, p0, p1);
     require(d_sino != nullptr, "sinogram pointer is null");
     if (inner_cg_iterations < 1) throw rk::ValidationError("admm inner_cg_iterations must be at least 1");
-    auto h = std::make_unique<rk_admm_state>();
+    std::unique_ptr<rk_admm_state> h(
+        admm_take_idle(&plan->p, &shearlet->s, dtype, batch, float(p0), float(p1), inner_cg_iterations));
+    if (!h) h = std::make_unique<rk_admm_state>();
     rk::Admm& a = h->a;
     a.plan = &plan->p;
     a.sh = &shearlet->s;
@@ -738,9 +801,13 @@ int rk_admm_read(rk_admm_state* admm, int which, int dtype, void* d_dst, void* s
 int rk_admm_destroy(rk_admm_state* admm) {
   return guarded_named(__func__, [&] {
     if (!admm) return;
+    // every stream that may still touch the state (a trailing rk_admm_read on the caller's)
     if (cudaSetDevice(admm->a.plan->device) == cudaSuccess) cudaDeviceSynchronize();
     cudaGetLastError();
-    delete admm;
+    if (admm->a.failed < 0)
+      admm_release(admm);  // healthy: kept for the next compatible call
+    else
+      delete admm;
     cudaGetLastError();
   });
 }

@@ -266,3 +266,29 @@ def test_graph_replay_equals_direct_launches(rk, port, cuda, monkeypatch):
     with pytest.raises(rk.DivergenceError) as e:
         rk.admm_reconstruct(op, plan, y, rk.AdmmParams(outer_iterations=5, p0=1e30))
     assert e.value.iteration == 0
+
+
+def test_repeated_calls_reuse_state_bitwise(rk, port, cuda):
+    """A finished ADMM's buffers and captured graph are kept for the next compatible call
+    (capi.cpp admm_take_idle): repeated calls, interleaved with an incompatible one (other
+    penalties) and a different batch, return bit-identical results; a shearlet plan freed
+    while a state built on it is idle does not leave a dangling state behind."""
+    import gc
+
+    s, na = 32, 24
+    g = rk.make_parallel(s, limited_angles(na))
+    op = rk.projector_operator(g)
+    y = rk.forward(g, dev(np.concatenate([phantom(port, s, np.float32)] * 3), cuda))
+    plan = rk.make_plan(s, s, [0.5, 0.5])
+    prm = rk.AdmmParams(p0=0.5, p1=0.1, outer_iterations=4, inner_cg_iterations=5)
+    first = rk.admm_reconstruct(op, plan, y, prm)
+    other = rk.admm_reconstruct(op, plan, y, rk.AdmmParams(p0=0.7, p1=0.1, outer_iterations=4, inner_cg_iterations=5))
+    single = rk.admm_reconstruct(op, plan, y[:1], prm)
+    again = rk.admm_reconstruct(op, plan, y, prm)
+    assert torch.equal(first, again)
+    assert torch.equal(single[0], first[0])
+    assert not torch.equal(other, first)
+    del plan
+    gc.collect()
+    plan2 = rk.make_plan(s, s, [0.5, 0.5])
+    assert torch.equal(rk.admm_reconstruct(op, plan2, y, prm), first)
