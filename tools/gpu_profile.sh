@@ -26,3 +26,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fil
 timeout 600 python tools/shard_probe.py par512 > gpurun_out/shard_probe_${TAG}_par.json 2>&1; tail -c 400 gpurun_out/shard_probe_${TAG}_par.json; echo
 timeout 600 python tools/b1_probe.py > gpurun_out/b1_probe_${TAG}.json 2>&1; tail -c 300 gpurun_out/b1_probe_${TAG}.json; echo
 timeout 600 python tools/fbp_probe.py > gpurun_out/fbp_probe_${TAG}.json 2>&1; tail -c 300 gpurun_out/fbp_probe_${TAG}.json; echo
+# summarise the captures on the box and drop the reports (gpurun copies back <= 64 MiB)
+for t in par fan h8 filter; do
+  if [ -f gpurun_out/prof_${TAG}_$t.ncu-rep ]; then
+    python tools/ncu_summary.py gpurun_out/prof_${TAG}_$t.ncu-rep $( [ $t = par ] && echo gpurun_out/launches_$TAG.csv ) > gpurun_out/ncu_summary_${TAG}_$t.md 2>&1
+    [ "${KEEP_REPS:-0}" = 1 ] || rm -f gpurun_out/prof_${TAG}_$t.ncu-rep
+  fi
+done
