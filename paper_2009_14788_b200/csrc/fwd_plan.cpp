@@ -408,6 +408,8 @@ void build_forward_plan(Plan& p, const std::vector<RayD>& rays, std::vector<floa
   ForwardSchedule& F = p.fwd;
   // Checks and diagnostics of the final schedule (planned or from the cache).
   auto finish = [&]() {
+    F.any_narrow = false;
+    for (const int4& c : F.cta) F.any_narrow |= ((c.z >> 5) & 7) != 0;
     if (const char* ve = std::getenv("RK_VERIFY_PLAN"); ve && ve[0] == '1') verify_forward_schedule(p, ray_geom, ray_aux);
     if (const char* me = std::getenv("RK_PLAN_MODEL"); me && me[0] == '1') {
       const auto w = model_wavefronts(p, ray_geom, ray_aux);

@@ -242,7 +242,9 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // for bit.
 // H8 (fp16 storage, batch > 1): half8 texels, eight images per lane, each tap
 // load converted to fp32 pairs; per image the same operations and order.
-template <class TOut, bool LANE, bool H8 = false>
+// NW: the schedule holds narrow-warp CTAs (ForwardSchedule::any_narrow); the
+// lane check is compiled in only then (it costs the half8 loop ~3 %).
+template <class TOut, bool LANE, bool H8, bool NW>
 __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
@@ -262,7 +264,9 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
   const int lq = (cfg.z >> 3) & 3;
   int slot = warp, k;
   if (lq == 0) {
+    // narrow-warp CTAs (coarse detectors, fwd_plan.cpp, cfg.z bits 5-7): lanes >= 32 >> n idle
     k = __ldg(warps + cta * (kFwdThreads / 32) + warp).y + lane;
+    if (NW && (lane >> (5 - ((cfg.z >> 5) & 7))) != 0) k = nd;
   } else {
     const int t = threadIdx.x;
     const int cq = t & ((8 >> lq) - 1), aq = (t >> (3 - lq)) & ((1 << lq) - 1);
@@ -271,8 +275,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     k = __ldg(warps + cta * (kFwdThreads / 32)).y + cg * (8 >> lq) + cq;
   }
   const int a = __ldg(warps + cta * (kFwdThreads / 32) + slot).x;
-  // narrow-warp CTAs (coarse detectors, fwd_plan.cpp): lanes >= 32 >> n idle
-  const bool valid = a >= 0 && k < nd && (lq != 0 || lane < (32 >> ((cfg.z >> 5) & 7)));
+  const bool valid = a >= 0 && k < nd;
   const int64_t r = int64_t(a) * nd + k;
   // Per-chunk layout chosen by the planner against bank conflicts (box record
   // z = pitch | orientation << 16 | per-lane tap order << 17): chunks of
@@ -524,7 +527,10 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   Cell* smem = reinterpret_cast<Cell*>(smem_raw);
   // this tile's staged cells per angle, and as many angles per pass as fit
   const int window = __ldg(tile_window + blockIdx.y * gridDim.x + blockIdx.x);
-  const int wc = window >> 1;  // middle cell (fp32 kinds measure kf from it)
+  // middle cell: the fp32 kinds measure kf from it (fp32 / fp64 storage; the fp16-storage
+  // kernels keep the window-start origin — their tolerance is 1e-3 and they are issue-bound)
+  constexpr bool kCentred = (KIND == kBpParallel || KIND == kBpFan32) && !std::is_same<TOut, __half>::value;
+  const int wc = kCentred ? window >> 1 : 0;
   const int chunk = min(kMaxBpChunk, cells / window);
   Cell* win = smem;                                                    // chunk * window <= cells
   Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kMaxBpChunk records
@@ -686,7 +692,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
       const Const k = cst[q];
       // fp32 kinds: kf relative to the middle cell wc of the window (half the magnitude, half the
       // fp32 rounding of kf); the pointer carries the offset back
-      const Cell* w = win + q * window + ((KIND == kBpParallel || KIND == kBpFan32) ? wc : 0);
+      const Cell* w = win + q * window + wc;
       // parallel: the column term is shared by the thread's pixels (one column);
       // fan (fp32 map): the row terms (a thread's pixels share one row)
       float col0 = 0.f, nrow = 0.f, drow = 0.f;
@@ -748,8 +754,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
           fk = float(fd);
           wt = float(kd - fd);
         }
-        constexpr bool centred = KIND == kBpParallel || KIND == kBpFan32;
-        const int c0 = min(max(int(fk), centred ? -wc : 0), window - 2 - (centred ? wc : 0));
+        const int c0 = min(max(int(fk), -wc), window - 2 - wc);
         const float wl = 1.f - wt;
         if constexpr (LANE) {
           const float s0 = w[c0], s1 = w[c0 + 1];
@@ -921,9 +926,11 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     const bool lane = single_lane(batch);
-    auto kern = lane ? forward_kernel<T, true> : forward_kernel<T, false>;
+    const bool nw = F.any_narrow;
+    auto kern = lane ? (nw ? forward_kernel<T, true, false, true> : forward_kernel<T, true, false, false>)
+                     : (nw ? forward_kernel<T, false, false, true> : forward_kernel<T, false, false, false>);
     if constexpr (std::is_same<T, __half>::value)
-      if (h8) kern = forward_kernel<T, false, true>;
+      if (h8) kern = nw ? forward_kernel<T, false, true, true> : forward_kernel<T, false, true, false>;
     const size_t smem = size_t(F.max_box) * (lane ? 2 * sizeof(float) : sizeof(float4));
     allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FORWARD, st);

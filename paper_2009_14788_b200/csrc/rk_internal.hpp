@@ -90,6 +90,7 @@ struct ForwardSchedule {
   int64_t max_box = 0;             // largest rows * pitch over all boxes (float4 cells)
   int64_t staged_texels = 0;       // per image group, all CTAs and chunks
   bool any_transposed = false;
+  bool any_narrow = false;         // some CTA runs narrow warps (cfg.z bits 5-7 nonzero)
   double sim_cost = 0.0, sim_ideal = 0.0;  // planner's simulated shared-memory wavefronts (chosen, conflict-free)
   bool from_cache = false;                 // loaded from the on-disk schedule cache (plan_cache.cpp)
   int mapping_count[4] = {0, 0, 0, 0};      // CTAs per lane mapping (log2 angles per quarter warp)
