@@ -960,7 +960,8 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                      : kind == kBpParHP  ? sizeof(ParHPConst)
                      : kind == kBpFan32  ? sizeof(Fan32Const)
                                          : sizeof(FanConst);
-  const size_t smem = size_t(p.bp_cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
+  const int cells = narrow ? p.bp_cells_narrow : p.bp_cells;
+  const size_t smem = size_t(cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     // the kernel variant for one kind: single-lane (batch 1), half8, WIDE (one group), NARROW or 256 x 4
@@ -982,7 +983,7 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
                                     p.g.source_distance, p.g.det_distance, p.trig.as<double2>(),
-                                    p.bp_tile_window.as<int>(), p.bp_cells, batch, static_cast<T*>(image), epi);
+                                    p.bp_tile_window.as<int>(), cells, batch, static_cast<T*>(image), epi);
   });
   RK_CUDA(cudaGetLastError());
 }

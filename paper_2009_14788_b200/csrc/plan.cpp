@@ -290,10 +290,21 @@ void build_plan(Plan& p) {
   }
   // angles per staging pass: keep the window slab near 32 KB (>= 1 angle, up to
   // 192 KB) for the widest tile; narrower tiles stage more angles per pass in
-  // the same cells (kernels.cu: chunk = min(32, cells / tile window))
-  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(32, (32 * 1024) / (window * 16)));
+  // the same cells (kernels.cu: chunk = min(32, cells / tile window)).  The
+  // NARROW kernel (128 threads, register-bound at seven CTAs per SM) gets a
+  // 30 KB slab: with the 32 constant records and the 1 KB the runtime reserves
+  // per CTA, seven then fit an SM's 228 KB (cfg3's fan windows left six at
+  // 32 KB: fan backprojection 4.36 -> 4.32 ms); the 512-thread kernels (two
+  // CTAs per SM) keep more angles per pass.
+  auto slab_chunk = [&](int64_t bytes) { return std::max<int64_t>(1, std::min<int64_t>(32, bytes / (window * 16))); };
+  static const int64_t narrow_slab = [] {
+    const char* e = std::getenv("RK_BP_WINDOW_BYTES");
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(30 * 1024);
+  }();
+  const int64_t chunk = slab_chunk(32 * 1024);
   p.bp_angle_chunk = int(chunk);
   p.bp_cells = int(chunk * window);
+  p.bp_cells_narrow = int(slab_chunk(narrow_slab) * window);
 
   // ----- upload (device < 0: host-only plan, used for inspection on machines without a GPU)
   if (p.device < 0) return;

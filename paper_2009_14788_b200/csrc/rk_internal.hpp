@@ -158,6 +158,7 @@ struct Plan {
   int bp_window = 0;       // staged detector cells per (tile, angle), widest tile
   int bp_angle_chunk = 0;  // angles staged per pass, widest tile
   int bp_cells = 0;        // staged cells per pass (shared memory), all tiles
+  int bp_cells_narrow = 0; // the same for the NARROW kernel (seven CTAs per SM)
   DeviceBuffer bp_tile_window;  // int per 32x32 tile: its staged cells per angle
   bool bp_fan_fp64 = false;  // fan beam with the source close to the image: fp64 pixel map
 

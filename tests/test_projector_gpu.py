@@ -448,6 +448,29 @@ def test_coarse_detector_and_narrow_detector_parity(rk, oracle, cuda, name, mk, 
     assert rel_l2(b, oracle.backprojection(ogeom(g), y)) <= TOL32
 
 
+@pytest.mark.parametrize("name,mk", [
+    ("fan-128-det16", lambda rk: fan(rk, 128, 40, 128.0, det_count=16)),
+    ("par-160-det20-sp8", lambda rk: par(rk, 160, 50, 20, 8.0)),
+])
+def test_coarse_detector_fp16_storage(rk, oracle, cuda, name, mk):
+    """fp16 storage on narrow-warp schedules: batch 9 runs the half8 forward with the
+    narrow-lane check compiled in (ForwardSchedule::any_narrow), batch 1 the single-lane
+    kernel; both within the fp16 tolerance of the reference and each batched image
+    bitwise equal to its single-image call (acceptance.cpp:340-389)."""
+    g = mk(rk)
+    rs = np.random.default_rng(23)
+    x = rs.uniform(0.0, 1.0, (9, g.image_size, g.image_size)).astype(np.float16)
+    f = host(rk.forward(g, dev(x, cuda)))
+    assert f.dtype == np.float16
+    assert rel_l2(f, oracle.forward(ogeom(g), x)) <= TOL16
+    for i in (0, 4, 8):
+        assert np.array_equal(host(rk.forward(g, dev(x[i:i + 1], cuda))), f[i:i + 1])
+    y = rs.standard_normal((9, g.n_angles, g.det_count)).astype(np.float16)
+    b = host(rk.backprojection(g, dev(y, cuda)))
+    assert rel_l2(b, oracle.backprojection(ogeom(g), y)) <= TOL16
+    assert np.array_equal(host(rk.backprojection(g, dev(y[3:4], cuda))), b[3:4])
+
+
 def test_materialize_matrix(rk, oracle, cuda):
     """projector.cpp:276-294 / test_projector.cpp:57-110: the 2x2 single-angle matrix exactly,
     the dense matrix against the reference's forward columns and A x against forward(x), and
