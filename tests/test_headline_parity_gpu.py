@@ -125,6 +125,28 @@ def test_headline_fp16_storage(rk, oracle, cuda, imgs, name, mk):
     assert np.sqrt(np.sum(d * d) / np.sum(ref_big.astype(np.float64)[fin] ** 2)) <= TOL16
 
 
+@pytest.mark.parametrize("name,mk", CONFIGS, ids=[c[0] for c in CONFIGS])
+def test_headline_fp64_storage(rk, oracle, cuda, imgs, name, mk):
+    """fp64 storage (projector.cpp:207-224: the output keeps the input precision): the inputs are
+    narrowed to fp32 on the pack, the kernels compute in fp32 and the results are widened on the
+    store, so the fp32 bar holds against the reference's fp64 arithmetic, and two of the four
+    images (batch 2 vs the batch-4 call) are bitwise equal."""
+    g = mk(rk)
+    og = ogeom(g)
+    xd = imgs.astype(np.float64)
+    sino = host(rk.forward(g, dev(xd, cuda)))
+    assert sino.dtype == np.float64
+    ref_sino = oracle.forward(og, xd)
+    for e in range(N_IMG):
+        assert rel_l2(sino[e], ref_sino[e]) <= TOL32, (name, e)
+    assert np.array_equal(host(rk.forward(g, dev(xd[1:3], cuda))), sino[1:3])
+    bp = host(rk.backprojection(g, dev(ref_sino, cuda)))
+    assert bp.dtype == np.float64
+    ref_bp = oracle.backprojection(og, ref_sino)
+    for e in range(N_IMG):
+        assert rel_l2(bp[e], ref_bp[e]) <= TOL32, (name, e)
+
+
 def test_cfg4_fbp_forward_sinogram_fp32(rk, oracle, cuda):
     """SURVEY 8d config 4's input is the oracle forward of the phantom batch; its FBP is checked on
     that sinogram in test_filter_solvers_gpu.py.  Here the GPU's own forward at 1024^2 / 720 angles
