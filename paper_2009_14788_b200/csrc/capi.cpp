@@ -82,6 +82,20 @@ struct ScratchLease {
   ~ScratchLease() { cudaEventRecord(p.scratch_free, st); }
 };
 
+// The same for a shearlet plan's spectra scratch (work_a / work_b), which the
+// analysis / synthesis calls and every ADMM state built on the plan share.
+struct ShearletLease {
+  rk::Shearlet& s;
+  cudaStream_t st;
+  std::lock_guard<std::mutex> lock;
+  ShearletLease(rk::Shearlet& sh, cudaStream_t stream) : s(sh), st(stream), lock(sh.mu) {
+    rk::set_device(s.device);
+    if (!s.scratch_free) RK_CUDA(cudaEventCreateWithFlags(&s.scratch_free, cudaEventDisableTiming));
+    RK_CUDA(cudaStreamWaitEvent(st, s.scratch_free, 0));
+  }
+  ~ShearletLease() { cudaEventRecord(s.scratch_free, st); }
+};
+
 size_t packed_image_bytes(const rk::Plan& p, int64_t batch) {
   return size_t(rk::groups_of(batch)) * size_t(p.s + 2) * size_t(p.s + 2) * sizeof(float4);
 }
@@ -689,8 +703,7 @@ int rk_shearlet_forward(rk_shearlet* plan, int dtype, const void* d_image, int64
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
-    std::lock_guard<std::mutex> lock(plan->s.mu);
-    rk::set_device(plan->s.device);
+    ShearletLease lease(plan->s, as_stream(stream));
     rk::shearlet_forward(plan->s, dtype, d_image, batch, d_coeff, as_stream(stream));
   });
 }
@@ -703,8 +716,7 @@ int rk_shearlet_backward(rk_shearlet* plan, int dtype, const void* d_coeff, int6
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_image != nullptr && d_coeff != nullptr, "image / coefficient pointer is null");
-    std::lock_guard<std::mutex> lock(plan->s.mu);
-    rk::set_device(plan->s.device);
+    ShearletLease lease(plan->s, as_stream(stream));
     rk::shearlet_backward(plan->s, dtype, d_coeff, batch, d_image, as_stream(stream));
   });
 }
@@ -763,7 +775,7 @@ int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* 
     a.inner = inner_cg_iterations;
     const std::vector<double> th = admm_thresholds(shearlet->s, weights, p0, p1);
     ScratchLease lease(plan->p, as_stream(stream));
-    std::lock_guard<std::mutex> lock(shearlet->s.mu);
+    ShearletLease sh_lease(shearlet->s, as_stream(stream));
     rk::admm_init(a, d_sino, th, as_stream(stream));
     *out = h.release();
   });
@@ -777,7 +789,7 @@ int rk_admm_iterate(rk_admm_state* admm, int64_t n, int64_t* failed_iteration, v
     int64_t failed = a.failed;
     if (failed < 0 && n > 0) {
       ScratchLease lease(*a.plan, as_stream(stream));
-      std::lock_guard<std::mutex> lock(a.sh->mu);
+      ShearletLease sh_lease(*a.sh, as_stream(stream));
       failed = rk::admm_iterate(a, n, as_stream(stream));
     }
     if (failed_iteration) *failed_iteration = failed;

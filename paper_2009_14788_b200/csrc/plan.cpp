@@ -38,6 +38,10 @@ Plan::~Plan() {
   if (scratch_free) cudaEventDestroy(scratch_free);
 }
 
+Shearlet::~Shearlet() {
+  if (scratch_free) cudaEventDestroy(scratch_free);
+}
+
 HostPipeline::~HostPipeline() {
   for (auto& s : streams)
     if (s) cudaStreamDestroy(s);

@@ -203,6 +203,13 @@ struct Shearlet {
   DeviceBuffer g_mult2, g_twiddle, g_mult2_64, g_twiddle64;
   DeviceBuffer work_a, work_b;      // spectra scratch
   std::mutex mu;
+  // work_a / work_b reuse across streams: every enqueue waits on and records
+  // this event (capi.cpp ShearletLease; created on first device use)
+  cudaEvent_t scratch_free = nullptr;
+  Shearlet() = default;
+  Shearlet(const Shearlet&) = delete;
+  Shearlet& operator=(const Shearlet&) = delete;
+  ~Shearlet();
 };
 // stored != nullptr: n_coeff x h x w multipliers from a plan cache, used verbatim
 void build_shearlet(Shearlet& sp, int64_t height, int64_t width, const std::vector<double>& alphas,
