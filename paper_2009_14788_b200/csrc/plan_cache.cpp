@@ -15,6 +15,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <cerrno>
 #include <cstdio>
 #include <cstdlib>
@@ -171,7 +172,10 @@ void store_schedule(const std::string& path, const std::vector<unsigned char>& k
   if (path.empty()) return;
   const std::string dir = path.substr(0, path.rfind('/'));
   if (!make_dirs(dir)) return;
-  const std::string tmp = path + ".tmp." + std::to_string(long(getpid()));
+  // one temporary file per writer (threads of one process may plan the same
+  // geometry at once): the rename then publishes only complete files
+  static std::atomic<unsigned> serial{0};
+  const std::string tmp = path + ".tmp." + std::to_string(long(getpid())) + "." + std::to_string(serial.fetch_add(1));
   FILE* f = std::fopen(tmp.c_str(), "wb");
   if (!f) return;
   const int32_t any_tr = F.any_transposed ? 1 : 0;

@@ -97,3 +97,30 @@ def test_warm_cache_is_fast_at_config2(rk, cache_dir):
     assert b.info()["schedule_from_cache"] and a.prepare() == b.prepare()
     # the warm plan still builds the fp64 ray table and backprojection windows; the schedule is read
     assert warm < 0.25 * cold, (cold, warm)
+
+
+def test_concurrent_writers_publish_complete_files(rk, cache_dir):
+    """Threads planning one geometry at once each write their own temporary file (plan_cache.cpp
+    store_schedule) and rename it into place: every plan gets the same schedule, the published
+    file loads, and no temporary file is left behind."""
+    import threading
+
+    g = rk.make_parallel(64, rk.angles_linspace(0.0, np.pi, 40))
+    digests, errs = [], []
+
+    def work():
+        try:
+            digests.append(Plan(g, 1.0, -1).prepare())
+        except BaseException as e:  # noqa: BLE001 (re-raised below)
+            errs.append(e)
+
+    ts = [threading.Thread(target=work) for _ in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs and len(set(digests)) == 1
+    assert len(glob.glob(os.path.join(cache_dir, "fwd_*.rkfs"))) == 1
+    assert not glob.glob(os.path.join(cache_dir, "*.tmp.*"))
+    p = Plan(g, 1.0, -1)
+    assert p.info()["schedule_from_cache"] and p.prepare() == digests[0]
