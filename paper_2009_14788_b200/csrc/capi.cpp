@@ -116,7 +116,23 @@ void check_device_filter(const rk_filter* f) {
 }
 
 // Device-pointer bodies, reused by the host-buffer pipelines with their own scratch.
-void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
+// One launch covers at most 65535 packed groups (the kernels' grid.y / grid.z);
+// larger batches run as consecutive sub-batches (results are per image, so
+// bit-identical to one launch).
+constexpr int64_t kMaxLaunchBatch = int64_t(65535) * rk::kPack;
+
+template <class F>
+void for_sub_batches(int64_t batch, F&& f) {
+  for (int64_t b0 = 0; b0 < batch; b0 += kMaxLaunchBatch) f(b0, std::min(kMaxLaunchBatch, batch - b0));
+}
+const void* advance(const void* ptr, int64_t items, size_t item_bytes) {
+  return static_cast<const char*>(ptr) + size_t(items) * item_bytes;
+}
+void* advance(void* ptr, int64_t items, size_t item_bytes) {
+  return static_cast<char*>(ptr) + size_t(items) * item_bytes;
+}
+
+void forward_launch(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
                   rk::DeviceBuffer& pkt, cudaStream_t st) {
   rk::ensure_forward_schedule(p);
   pk.reserve(packed_image_bytes(p, batch));
@@ -133,8 +149,8 @@ void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, vo
   rk::launch_forward(p, pk.as<float4>(), pkt.as<float4>(), batch, dtype, d_sino, st);
 }
 
-void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
-                      rk::DeviceBuffer& pk, cudaStream_t st) {
+void backproject_launch(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
+                        rk::DeviceBuffer& pk, cudaStream_t st) {
   pk.reserve(packed_sino_bytes(p, batch));
   if (rk::use_h8(dtype, batch))
     rk::launch_pack_sino_h8(d_sino, batch, p.na, p.nd, pk.as<float4>(), st);
@@ -143,12 +159,51 @@ void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch,
   rk::launch_backproject(p, pk.as<float4>(), batch, dtype, d_image, st);
 }
 
-void fbp_into(rk::Plan& p, rk::Filter& f, int dtype, const void* d_sino, int64_t batch, void* d_image,
-              rk::DeviceBuffer& pk, cudaStream_t st) {
+void fbp_launch(rk::Plan& p, rk::Filter& f, int dtype, const void* d_sino, int64_t batch, void* d_image,
+                rk::DeviceBuffer& pk, cudaStream_t st) {
   pk.reserve(packed_sino_bytes(p, batch));
   // the filter writes straight into the packed layout the backprojector reads
   rk::launch_filter(f, dtype, d_sino, batch, p.na, nullptr, pk.as<float4>(), st);
   rk::launch_backproject(p, pk.as<float4>(), batch, dtype, d_image, st);
+}
+
+void forward_into(rk::Plan& p, int dtype, const void* d_image, int64_t batch, void* d_sino, rk::DeviceBuffer& pk,
+                  rk::DeviceBuffer& pkt, cudaStream_t st) {
+  const size_t es = rk::dtype_size(dtype), img = size_t(p.s * p.s) * es, sino = size_t(p.na * p.nd) * es;
+  for_sub_batches(batch, [&](int64_t b0, int64_t nb) {
+    forward_launch(p, dtype, advance(d_image, b0, img), nb, advance(d_sino, b0, sino), pk, pkt, st);
+  });
+}
+
+void backproject_into(rk::Plan& p, int dtype, const void* d_sino, int64_t batch, void* d_image,
+                      rk::DeviceBuffer& pk, cudaStream_t st) {
+  const size_t es = rk::dtype_size(dtype), img = size_t(p.s * p.s) * es, sino = size_t(p.na * p.nd) * es;
+  for_sub_batches(batch, [&](int64_t b0, int64_t nb) {
+    backproject_launch(p, dtype, advance(d_sino, b0, sino), nb, advance(d_image, b0, img), pk, st);
+  });
+}
+
+void fbp_into(rk::Plan& p, rk::Filter& f, int dtype, const void* d_sino, int64_t batch, void* d_image,
+              rk::DeviceBuffer& pk, cudaStream_t st) {
+  const size_t es = rk::dtype_size(dtype), img = size_t(p.s * p.s) * es, sino = size_t(p.na * p.nd) * es;
+  for_sub_batches(batch, [&](int64_t b0, int64_t nb) {
+    fbp_launch(p, f, dtype, advance(d_sino, b0, sino), nb, advance(d_image, b0, img), pk, st);
+  });
+}
+
+void filter_into(rk::Filter& f, int dtype, const void* d_in, int64_t batch, int64_t n_angles, void* d_out,
+                 cudaStream_t st) {
+  const size_t sino = size_t(n_angles * f.det_count) * rk::dtype_size(dtype);
+  for_sub_batches(batch, [&](int64_t b0, int64_t nb) {
+    rk::launch_filter(f, dtype, advance(d_in, b0, sino), nb, n_angles, advance(d_out, b0, sino), nullptr, st);
+  });
+}
+
+// the solvers and ADMM keep whole-batch packed state: one launch per operator
+void check_launch_batch(int64_t batch) {
+  if (batch > kMaxLaunchBatch)
+    throw rk::ValidationError("batch of " + std::to_string(batch) + " exceeds the solver limit of " +
+                              std::to_string(kMaxLaunchBatch) + " images per call; split the batch");
 }
 
 void check_dtype(int dtype) { (void)rk::dtype_size(dtype); }
@@ -491,7 +546,7 @@ int rk_filter_sinogram(rk_filter* filter, int dtype, const void* d_in, int64_t b
     rk::Filter& f = filter->f;
     std::lock_guard<std::mutex> lock(f.mu);
     rk::set_device(f.device);
-    rk::launch_filter(f, dtype, d_in, batch, n_angles, d_out, nullptr, as_stream(stream));
+    filter_into(f, dtype, d_in, batch, n_angles, d_out, as_stream(stream));
   });
 }
 
@@ -556,7 +611,7 @@ int rk_filter_sinogram_host(rk_filter* filter, int dtype, const void* h_in, int6
     const size_t item = size_t(n_angles * f.det_count) * rk::dtype_size(dtype);  // one sinogram
     run_host_pipeline(f.pipe, f.device, f.mu, batch, item, item, h_in, h_out, nullptr,
                       [&](const void* din, int64_t nb, void* dout, int, cudaStream_t st) {
-                        rk::launch_filter(f, dtype, din, nb, n_angles, dout, nullptr, st);
+                        filter_into(f, dtype, din, nb, n_angles, dout, st);
                       });
   });
 }
@@ -601,6 +656,7 @@ int rk_landweber(rk_plan* plan, int dtype, const void* d_y, const void* d_guess,
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_y != nullptr && d_guess != nullptr && d_x != nullptr, "landweber pointer is null");
+    check_launch_batch(batch);
     rk::Plan& p = plan->p;
     int failed = -1;
     {
@@ -622,6 +678,7 @@ int rk_cgne(rk_plan* plan, int dtype, const void* d_y, const void* d_guess, int6
     check_dtype(dtype);
     require(batch >= 1, "batch must be >= 1, got " + std::to_string(batch));
     require(d_y != nullptr && d_guess != nullptr && d_x != nullptr, "cgne pointer is null");
+    check_launch_batch(batch);
     rk::Plan& p = plan->p;
     int failed = -1;
     {
@@ -759,6 +816,7 @@ int rk_admm_create(rk_plan* plan, rk_shearlet* shearlet, int dtype, const void* 
     require(out != nullptr, "admm pointer is null");
     *out = nullptr;
     check_admm_args(plan, shearlet, dtype, batch, p0, p1);
+    check_launch_batch(batch);
     require(d_sino != nullptr, "sinogram pointer is null");
     if (inner_cg_iterations < 1) throw rk::ValidationError("admm inner_cg_iterations must be at least 1");
     std::unique_ptr<rk_admm_state> h(

@@ -3,10 +3,14 @@
 // pi / (2 n_angles) — sino_filter.cpp:98-124 (filtration always fp32,
 // :106-123).
 //
-// One CTA filters the four rows (b = 4g..4g+3, angle a) that share one
-// packed float4 sinogram cell, as two complex shared-memory FFTs: the
-// response is real and even, so for z = x + i y, IFFT(FFT(z) H) = x*h + i (y*h)
-// filters two real rows at once.  The forward transform is
+// One CTA filters four rows of one packed group — images 2r, 2r + 1 of the
+// group's four at an angle pair (a0, a0 + 1) — as two complex shared-memory
+// FFTs: the response is real and even, so for z = x + i y,
+// IFFT(FFT(z) H) = x*h + i (y*h) filters two real rows at once.
+// The two rows of a sequence are one image's rows at the two angles, never two
+// images': the complex butterflies mix the real and imaginary parts at the
+// rounding level, so pairing images made a row's result depend on its batch
+// neighbour (FBP of a batch differed from per-image calls in the last bit).  The forward transform is
 // decimation-in-frequency (natural in, bit-reversed out), the response is
 // applied in bit-reversed order, and the inverse is decimation-in-time with
 // conjugate twiddles (bit-reversed in, natural out): no permutation pass.
@@ -103,10 +107,11 @@ __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, 
 }
 
 // PACKED 0: user layout; 1: packed float4 cells (four images); 2: half of a
-// packed half8 cell (fp16 storage, use_h8): this CTA's four rows are images
-// 4g .. 4g+3, i.e. the low or high 8 bytes of group g / 2's cells.
+// packed half8 cell (fp16 storage, use_h8): this CTA's images 4g .. 4g+3 are
+// the low or high four halves of group g / 2's cells.
 //
-// Passes (P = 2^logP points, two complex sequences z = row_a + i row_b):
+// Round r = blockIdx.z (0, 1): sequence s is image q = 2r + s,
+// z = row(q, a0) + i row(q, a0 + 1) (zero when a0 + 1 = n_angles).  Passes (P = 2^logP points, two sequences):
 //   forward DIF: the first pass reads the rows from global memory (the upper
 //   half is the zero padding: not read, first layer pruned), the middle
 //   passes run in shared memory, the last pass multiplies by the response
@@ -122,51 +127,53 @@ __device__ __forceinline__ void filter_pass(int logn, int lh, const float2* tw, 
 // which the issue-bound passes need (ncu r2d: 79 % issue active); LOGP = 0
 // takes the size at run time.
 template <class TIn, class TOut, int PACKED, int LOGP>
-__global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __restrict__ in, int64_t batch, int na,
-                                                                int nd, int P_rt, int logP_rt,
-                                                                const float* __restrict__ resp,
-                                                                const float2* __restrict__ tw, float scale,
-                                                                TOut* __restrict__ out, float4* __restrict__ packed) {
+// CTAs per SM: four up to 2^11 points (64 registers: without the bound the half8
+// variant took 74 and three CTAs, +20 % at cfg4), three at 2^12 (64 KB of shared
+// memory each)
+__global__ void __launch_bounds__(kFilterThreads, (LOGP > 0 && LOGP <= 11) ? 4 : LOGP == 12 ? 3 : 1)
+    filter_kernel(const TIn* __restrict__ in, int64_t batch, int na, int nd, int P_rt, int logP_rt,
+                  const float* __restrict__ resp, const float2* __restrict__ tw, float scale, TOut* __restrict__ out,
+                  float4* __restrict__ packed) {
   const int logP = LOGP ? LOGP : logP_rt;
   const int P = LOGP ? (1 << LOGP) : P_rt;
   extern __shared__ float2 fsm[];
-  float2* za = fsm;  // rows q=0 (re) and q=1 (im), swizzled slots (fft_swz)
+  float2* za = fsm;  // sequences 0 and 1, swizzled slots (fft_swz)
   const float2* tws = tw;  // per-stage twiddle table (plan.cpp build_filter): consecutive per butterfly lane
-  const int a = blockIdx.x;
+  const int a0 = 2 * int(blockIdx.x);
+  const bool has1 = a0 + 1 < na;  // the pair's second angle (odd n_angles: the last pair has one)
   const int64_t g = blockIdx.y;
   const int shift = 32 - logP;
-  const TIn* rows[4];
-  bool valid[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t b = g * kPack + q;
-    valid[q] = b < batch;
-    rows[q] = in + (valid[q] ? (b * na + a) * int64_t(nd) : 0);
-  }
   auto sm_load = [&](int seq, int i, int) { return za[seq * P + fft_swz(i)]; };
   auto sm_store = [&](int seq, int i, int, float2 v) { za[seq * P + fft_swz(i)] = v; };
-  // sequence seq = rows 2 seq (re) and 2 seq + 1 (im); zero beyond det_count
-  // (selects, not rows[2 * seq]: a dynamic index would put the arrays in local memory)
-  auto gl_load = [&](int seq, int i, int) {
-    float re = 0.f, im = 0.f;
-    if (i < nd) {
-      const bool vre = seq ? valid[2] : valid[0], vim = seq ? valid[3] : valid[1];
-      const TIn* pre = seq ? rows[2] : rows[0];
-      const TIn* pim = seq ? rows[3] : rows[1];
-      if (vre) re = ld_f32(pre + i);
-      if (vim) im = ld_f32(pim + i);
-    }
-    return make_float2(re, im);
-  };
-  // ---- forward DIF (natural -> bit-reversed), fft_dif_seq's pass order
-  const int r0 = logP % 3 == 0 ? 3 : logP % 3;  // the short pass first, at the widest stride
-  int lh = logP - r0;
-  const bool single = lh == 0;  // one pass (P <= 8): it both reads the rows and applies the response
   auto mul_store = [&](int seq, int i, int, float2 v) {
     const int f = int(__brev(unsigned(i)) >> shift);
     const float h = __ldg(resp + (f <= P / 2 ? f : P - f));
     za[seq * P + fft_swz(i)] = make_float2(v.x * h, v.y * h);
   };
+  const float inv = 1.0f / float(P);
+  const int r0 = logP % 3 == 0 ? 3 : logP % 3;  // the short forward pass first, at the widest stride
+  // round = blockIdx.z: one CTA per round (a loop over both rounds kept values
+  // live across them: 116 registers)
+  const int round = int(blockIdx.z);
+  // sequence seq: image q = 2 round + seq of the group, rows (q, a0) (re) and (q, a0 + 1) (im)
+  const int64_t b0 = g * kPack + 2 * round, b1 = b0 + 1;
+  const bool v0 = b0 < batch, v1 = b1 < batch;
+  if (!v0) return;  // the group's remaining images are missing
+  const TIn* row0 = in + (b0 * na + a0) * int64_t(nd);
+  const TIn* row1 = in + (v1 ? (b1 * na + a0) * int64_t(nd) : 0);
+  // (selects, not arrays indexed by seq: a dynamic index would put them in local memory)
+  auto gl_load = [&](int seq, int i, int) {
+    float re = 0.f, im = 0.f;
+    if (i < nd && (seq ? v1 : v0)) {
+      const TIn* r = seq ? row1 : row0;
+      re = ld_f32(r + i);
+      if (has1) im = ld_f32(r + nd + i);
+    }
+    return make_float2(re, im);
+  };
+  // ---- forward DIF (natural -> bit-reversed), fft_dif_seq's pass order
+  int lh = logP - r0;
+  const bool single = lh == 0;  // one pass (P <= 8): it both reads the rows and applies the response
   if (r0 == 1) {
     if (single) filter_pass<1, true, false, true>(logP, lh, tws, gl_load, mul_store);
     else filter_pass<1, true, false, true>(logP, lh, tws, gl_load, sm_store);
@@ -187,24 +194,25 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
   }
   // ---- inverse DIT (bit-reversed -> natural), conjugate twiddles; the last
   // pass crops, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
-  const float inv = 1.0f / float(P);
   auto out_store = [&](int seq, int i, int, float2 v) {
-    if (i >= nd) return;
-    const float v0 = (v.x * inv) * scale, v1 = (v.y * inv) * scale;
+    if (i >= nd || !(seq ? v1 : v0)) return;
+    const int q = 2 * round + seq;
+    const float f0 = (v.x * inv) * scale, f1 = (v.y * inv) * scale;
     if (PACKED == 2) {
-      // two halves of this CTA's four: exactly the values the float4 path narrows through fp16
-      const unsigned bits = unsigned(__half_as_ushort(__float2half_rn(v0))) |
-                            (unsigned(__half_as_ushort(__float2half_rn(v1))) << 16);
-      reinterpret_cast<unsigned*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + i) * 4 + (g & 1) * 2 + seq] = bits;
+      // this CTA's four of the cell's eight halves: the values the float4 path narrows through fp16
+      __half* c = reinterpret_cast<__half*>(packed) + (((g >> 1) * na + a0) * int64_t(nd) + i) * 8 + (g & 1) * 4 + q;
+      c[0] = __float2half_rn(f0);
+      if (has1) c[int64_t(nd) * 8] = __float2half_rn(f1);
     } else if (PACKED == 1) {
       // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows
       // to the storage precision first (sino_filter.cpp:123, 126-128)
-      reinterpret_cast<float2*>(packed)[((g * na + a) * int64_t(nd) + i) * 2 + seq] =
-          make_float2(float(st_cast<TOut>(v0)), float(st_cast<TOut>(v1)));
+      float* c = reinterpret_cast<float*>(packed) + ((g * na + a0) * int64_t(nd) + i) * 4 + q;
+      c[0] = float(st_cast<TOut>(f0));
+      if (has1) c[int64_t(nd) * 4] = float(st_cast<TOut>(f1));
     } else {
-      const bool vre = seq ? valid[2] : valid[0], vim = seq ? valid[3] : valid[1];
-      if (vre) out[((g * kPack + 2 * seq) * na + a) * int64_t(nd) + i] = st_cast<TOut>(v0);
-      if (vim) out[((g * kPack + 2 * seq + 1) * na + a) * int64_t(nd) + i] = st_cast<TOut>(v1);
+      TOut* o = out + ((g * kPack + q) * na + a0) * int64_t(nd) + i;
+      o[0] = st_cast<TOut>(f0);
+      if (has1) o[nd] = st_cast<TOut>(f1);
     }
   };
   int lq = 0;
@@ -230,7 +238,8 @@ __global__ void __launch_bounds__(kFilterThreads) filter_kernel(const TIn* __res
 //   out[i] = a[i] + conj(W_P^i) b[i]   (only i < det_count <= P/2 is kept),
 // so after a cluster barrier each CTA reads the other's half through
 // distributed shared memory for its share of the outputs.  One complex
-// sequence (two rows) per cluster; P/2 complex in each CTA (64 / 128 KB).
+// sequence per cluster — image q = blockIdx.z of the group at the angle pair
+// (a0, a0 + 1), as in filter_kernel; P/2 complex in each CTA (64 / 128 KB).
 template <class TIn, class TOut, int PACKED, int LOGH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFilterThreads)
     filter_split_kernel(const TIn* __restrict__ in, int64_t batch, int na, int nd, const float* __restrict__ resp,
@@ -240,21 +249,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFilterThreads)
   extern __shared__ float2 fsm[];
   float2* za = fsm;  // this CTA's half, swizzled slots (fft_swz)
   const unsigned rank = blockIdx.x & 1u;  // cluster rank: 0 even, 1 odd frequencies
-  const int a = int(blockIdx.x >> 1);
+  const int a0 = 2 * int(blockIdx.x >> 1);
+  const bool has1 = a0 + 1 < na;
   const int64_t g = blockIdx.y;
-  const int seq = int(blockIdx.z);  // rows 2 seq (re) and 2 seq + 1 (im) of packed group g
-  const int64_t b_re = g * kPack + 2 * seq, b_im = b_re + 1;
-  const bool vre = b_re < batch, vim = b_im < batch;
-  const TIn* pre = in + (vre ? (b_re * na + a) * int64_t(nd) : 0);
-  const TIn* pim = in + (vim ? (b_im * na + a) * int64_t(nd) : 0);
+  const int q = int(blockIdx.z);  // image q of packed group g: rows (q, a0) (re) and (q, a0 + 1) (im)
+  const int64_t b = g * kPack + q;
+  if (b >= batch) return;  // both CTAs of the cluster leave together (same b)
+  const TIn* pre = in + (b * na + a0) * int64_t(nd);
   const float2* wP = tw + (H - 1);  // stage logP - 1: W_P^k, k < P/2
   auto sm_load = [&](int, int i, int) { return za[fft_swz(i)]; };
   auto sm_store = [&](int, int i, int, float2 v) { za[fft_swz(i)] = v; };
   auto gl_load = [&](int, int i, int) {  // y_rank[i]
     float re = 0.f, im = 0.f;
     if (i < nd) {
-      if (vre) re = ld_f32(pre + i);
-      if (vim) im = ld_f32(pim + i);
+      re = ld_f32(pre + i);
+      if (has1) im = ld_f32(pre + nd + i);
     }
     float2 v = make_float2(re, im);
     if (rank) v = fft_cmul(v, __ldg(wP + i));
@@ -298,15 +307,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFilterThreads)
     const float2 wb = fft_cmul_conj(bv, __ldg(wP + i));
     const float v0 = ((v.x + wb.x) * inv) * scale, v1 = ((v.y + wb.y) * inv) * scale;
     if (PACKED == 2) {
-      const unsigned bits = unsigned(__half_as_ushort(__float2half_rn(v0))) |
-                            (unsigned(__half_as_ushort(__float2half_rn(v1))) << 16);
-      reinterpret_cast<unsigned*>(packed)[(((g >> 1) * na + a) * int64_t(nd) + i) * 4 + (g & 1) * 2 + seq] = bits;
+      __half* c = reinterpret_cast<__half*>(packed) + (((g >> 1) * na + a0) * int64_t(nd) + i) * 8 + (g & 1) * 4 + q;
+      c[0] = __float2half_rn(v0);
+      if (has1) c[int64_t(nd) * 8] = __float2half_rn(v1);
     } else if (PACKED == 1) {
-      reinterpret_cast<float2*>(packed)[((g * na + a) * int64_t(nd) + i) * 2 + seq] =
-          make_float2(float(st_cast<TOut>(v0)), float(st_cast<TOut>(v1)));
+      float* c = reinterpret_cast<float*>(packed) + ((g * na + a0) * int64_t(nd) + i) * 4 + q;
+      c[0] = float(st_cast<TOut>(v0));
+      if (has1) c[int64_t(nd) * 4] = float(st_cast<TOut>(v1));
     } else {
-      if (vre) out[(b_re * na + a) * int64_t(nd) + i] = st_cast<TOut>(v0);
-      if (vim) out[(b_im * na + a) * int64_t(nd) + i] = st_cast<TOut>(v1);
+      TOut* o = out + (b * na + a0) * int64_t(nd) + i;
+      o[0] = st_cast<TOut>(v0);
+      if (has1) o[nd] = st_cast<TOut>(v1);
     }
   }
   cluster.sync();  // the other CTA may still read this one's half
@@ -331,10 +342,11 @@ void launch_filter(const Filter& f, int dtype, const void* in, int64_t batch, in
   while ((1 << logP) < P) ++logP;
   const size_t smem = size_t(2) * P * sizeof(float2);  // two sequences
   const float scale = float(M_PI / (2.0 * double(n_angles)));  // sino_filter.cpp:108
-  dim3 grid(unsigned(n_angles), unsigned(groups_of(batch)));
+  const unsigned pairs = unsigned((n_angles + 1) / 2);  // angle pairs (a0, a0 + 1)
+  dim3 grid(pairs, unsigned(groups_of(batch)), 2u);  // z: the round (image pair of the group)
   if (logP >= 14) {  // 2^14, 2^15 (det_count 4097 .. 16384): the two-CTA cluster kernel
     const size_t hsmem = size_t(P / 2) * sizeof(float2);
-    dim3 sgrid(unsigned(2 * n_angles), unsigned(groups_of(batch)), 2u);
+    dim3 sgrid(2 * pairs, unsigned(groups_of(batch)), unsigned(kPack));
     dispatch(dtype, [&](auto tag) {
       using T = decltype(tag);
       auto pick = [&](auto packed_tag) {

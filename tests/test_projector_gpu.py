@@ -501,3 +501,33 @@ def test_very_large_batch(rk, oracle, cuda):
     r = subprocess.run([sys.executable, __import__("os").path.join(root, "tools", "big_batch_probe.py"), "2049"],
                        capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_batch_beyond_one_launch(rk, oracle, cuda):
+    """262,145 tiny images: more packed groups than one launch's grid.y / grid.z holds (65,535),
+    so the device calls run consecutive sub-batches (capi.cpp for_sub_batches). Elements on both
+    sides of the launch boundary equal their single-image results bit for bit and the reference;
+    fp16 (half8 groups) too."""
+    g = rk.make_parallel(4, [0.3, 1.1, 2.0], 5)
+    B = 65535 * 4 + 5
+    rs = np.random.default_rng(3)
+    x = rs.uniform(0.0, 1.0, (B, 4, 4)).astype(np.float32)
+    xd = dev(x, cuda)
+    f = rk.forward(g, xd)
+    b = rk.backprojection(g, f)
+    fb = rk.fbp(g, f)
+    fs = rk.filter_sinogram(f, rk.make_filter("ram-lak", g.det_count))
+    torch.cuda.synchronize()
+    idx = [0, 65535 * 4 - 1, 65535 * 4, B - 1]
+    fh = host(f)
+    assert rel_l2(fh[idx], oracle.forward(ogeom(g), x[idx])) <= TOL32
+    for i in idx:
+        f1 = rk.forward(g, xd[i:i + 1])
+        assert torch.equal(f1, f[i:i + 1])
+        assert torch.equal(rk.backprojection(g, f1), b[i:i + 1])
+        assert torch.equal(rk.fbp(g, f1), fb[i:i + 1])
+    xh = x.astype(np.float16)
+    fh16 = rk.forward(g, dev(xh, cuda))
+    for i in idx:
+        assert torch.equal(rk.forward(g, dev(xh[i:i + 1], cuda)), fh16[i:i + 1])
+    assert np.isfinite(host(fs)).all()
