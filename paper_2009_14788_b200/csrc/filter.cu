@@ -194,37 +194,52 @@ __global__ void __launch_bounds__(kFilterThreads, (LOGP > 0 && LOGP <= 11) ? 4 :
   }
   // ---- inverse DIT (bit-reversed -> natural), conjugate twiddles; the last
   // pass crops, x 1/P (irfft normalisation, fft.cpp:117-118), x pi/(2 na)
+  // user layout: the last inverse pass writes the rows from registers
   auto out_store = [&](int seq, int i, int, float2 v) {
     if (i >= nd || !(seq ? v1 : v0)) return;
-    const int q = 2 * round + seq;
-    const float f0 = (v.x * inv) * scale, f1 = (v.y * inv) * scale;
-    if (PACKED == 2) {
-      // this CTA's four of the cell's eight halves: the values the float4 path narrows through fp16
-      __half* c = reinterpret_cast<__half*>(packed) + (((g >> 1) * na + a0) * int64_t(nd) + i) * 8 + (g & 1) * 4 + q;
-      c[0] = __float2half_rn(f0);
-      if (has1) c[int64_t(nd) * 8] = __float2half_rn(f1);
-    } else if (PACKED == 1) {
-      // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows
-      // to the storage precision first (sino_filter.cpp:123, 126-128)
-      float* c = reinterpret_cast<float*>(packed) + ((g * na + a0) * int64_t(nd) + i) * 4 + q;
-      c[0] = float(st_cast<TOut>(f0));
-      if (has1) c[int64_t(nd) * 4] = float(st_cast<TOut>(f1));
-    } else {
-      TOut* o = out + ((g * kPack + q) * na + a0) * int64_t(nd) + i;
-      o[0] = st_cast<TOut>(f0);
-      if (has1) o[nd] = st_cast<TOut>(f1);
-    }
+    TOut* o = out + ((g * kPack + 2 * round + seq) * na + a0) * int64_t(nd) + i;
+    o[0] = st_cast<TOut>((v.x * inv) * scale);
+    if (has1) o[nd] = st_cast<TOut>((v.y * inv) * scale);
   };
-  int lq = 0;
+  auto inverse = [&](auto last) {
+    int lq = 0;
 #pragma unroll
-  for (; lq + 3 <= logP; lq += 3) {
-    if (lq + 3 == logP)
-      filter_pass<3, false, true, false>(logP, lq, tws, sm_load, out_store);
-    else
-      filter_pass<3, false, true, false>(logP, lq, tws, sm_load, sm_store);
+    for (; lq + 3 <= logP; lq += 3) {
+      if (lq + 3 == logP)
+        filter_pass<3, false, true, false>(logP, lq, tws, sm_load, last);
+      else
+        filter_pass<3, false, true, false>(logP, lq, tws, sm_load, sm_store);
+    }
+    if (logP - lq == 2) filter_pass<2, false, true, false>(logP, lq, tws, sm_load, last);
+    if (logP - lq == 1) filter_pass<1, false, true, false>(logP, lq, tws, sm_load, last);
+  };
+  if constexpr (PACKED == 0) {
+    inverse(out_store);
+  } else {
+    // packed cells: the two sequences (images 2 round, 2 round + 1) share each cell, so the
+    // last pass leaves them in shared memory and one thread writes both lanes per (angle, cell)
+    // — 8-byte float2 / 4-byte half2 stores instead of two scalar ones
+    inverse(sm_store);
+    for (int i = threadIdx.x; i < nd; i += kFilterThreads) {
+      const float2 z0 = za[fft_swz(i)], z1 = za[P + fft_swz(i)];  // (re, im) = (angle a0, a0 + 1)
+      // fbp = backprojection(filter_sinogram(sino)) narrows the filtered rows to the
+      // storage precision first (sino_filter.cpp:123, 126-128); a missing image's lane gets 0
+      auto narrow = [&](float v) { return float(st_cast<TOut>((v * inv) * scale)); };
+      const float r00 = narrow(z0.x), r01 = v1 ? narrow(z1.x) : 0.f;  // angle a0
+      const float r10 = narrow(z0.y), r11 = v1 ? narrow(z1.y) : 0.f;  // angle a0 + 1
+      if (PACKED == 2) {
+        // this CTA's two of the cell's eight halves: the values the float4 path narrows through fp16
+        __half2* c =
+            reinterpret_cast<__half2*>(packed) + (((g >> 1) * na + a0) * int64_t(nd) + i) * 4 + (g & 1) * 2 + round;
+        c[0] = __floats2half2_rn(r00, r01);
+        if (has1) c[int64_t(nd) * 4] = __floats2half2_rn(r10, r11);
+      } else {
+        float2* c = reinterpret_cast<float2*>(packed) + ((g * na + a0) * int64_t(nd) + i) * 2 + round;
+        c[0] = make_float2(r00, r01);
+        if (has1) c[int64_t(nd) * 2] = make_float2(r10, r11);
+      }
+    }
   }
-  if (logP - lq == 2) filter_pass<2, false, true, false>(logP, lq, tws, sm_load, out_store);
-  if (logP - lq == 1) filter_pass<1, false, true, false>(logP, lq, tws, sm_load, out_store);
 }
 
 // Transforms of P = 2^14 and 2^15 points (det_count 4097 .. 16384) no longer
