@@ -244,7 +244,9 @@ constexpr int kFwdThreads = 256;  // A = 8 angles (warps) x W = 32 detectors (la
 // load converted to fp32 pairs; per image the same operations and order.
 // NW: the schedule holds narrow-warp CTAs (ForwardSchedule::any_narrow); the
 // lane check is compiled in only then (it costs the half8 loop ~3 %).
-template <class TOut, bool LANE, bool H8, bool NW>
+// CM: grid (groups, CTAs) instead of (CTAs, groups) — CTA-major launch order for few groups
+// (launch_forward); a template flag because any change to the half8 loop's code costs it ~1 %.
+template <class TOut, bool LANE, bool H8, bool NW, bool CM>
 __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     const float4* __restrict__ img, const float4* __restrict__ img_t, int s, const float4* __restrict__ ray_geom,
     const float4* __restrict__ ray_aux, const int4* __restrict__ boxes, const int4* __restrict__ cta_cfg,
@@ -252,8 +254,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_kernel(
     int lane_box) {
   extern __shared__ float4 box_s[];
   __shared__ unsigned long long box_bar;  // TMA completion of the current chunk's box
-  const int cta = blockIdx.x;
-  const int64_t g = blockIdx.y;
+  // grid (CTAs, groups), or (groups, CTAs) for few groups: the launch order then follows the
+  // planner's longest-first CTA order across all groups, not group after group (launch_forward)
+  const int cta = CM ? blockIdx.y : blockIdx.x;
+  const int64_t g = CM ? blockIdx.x : blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 cfg = __ldg(cta_cfg + cta);  // {first box, boxes, flags}
   // lane -> ray, chosen by the planner against bank conflicts (angles are
@@ -922,15 +926,34 @@ void launch_forward(const Plan& p, const float4* packed_image, const float4* pac
                     int dtype, void* sino, cudaStream_t st, FwdEpilogue epi) {
   const ForwardSchedule& F = p.fwd;
   const bool h8 = epi.mode == kOutUser && use_h8(dtype, batch);
-  dim3 grid(unsigned(F.cta.size()), unsigned(h8 ? groups_of_h8(batch) : groups_of(batch)));
+  const int64_t groups = h8 ? groups_of_h8(batch) : groups_of(batch);
+  // few groups (small batches, e.g. a rank's shard): CTA-major launch order, so the longest
+  // CTAs of every group start first and the last wave holds the shortest; with many groups
+  // group-major order keeps one group's image in L2 while its CTAs run
+  static const int64_t cta_major_groups = [] {
+    const char* e = std::getenv("RK_FWD_CTA_MAJOR_GROUPS");
+    return e ? int64_t(std::atoll(e)) : int64_t(8);
+  }();
+  const bool cta_major = !single_lane(batch) && groups <= cta_major_groups && F.cta.size() <= 65535;
+  const dim3 grid = cta_major ? dim3(unsigned(groups), unsigned(F.cta.size()))
+                              : dim3(unsigned(F.cta.size()), unsigned(groups));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     const bool lane = single_lane(batch);
     const bool nw = F.any_narrow;
-    auto kern = lane ? (nw ? forward_kernel<T, true, false, true> : forward_kernel<T, true, false, false>)
-                     : (nw ? forward_kernel<T, false, false, true> : forward_kernel<T, false, false, false>);
+    // the variant for (single lane, half8): narrow-lane check and launch order from the schedule
+    auto pick = [&](auto lane_tag, auto h8_tag) {
+      constexpr bool L = decltype(lane_tag)::value, H = decltype(h8_tag)::value;
+      if constexpr (L) {
+        return nw ? forward_kernel<T, L, H, true, false> : forward_kernel<T, L, H, false, false>;
+      } else {
+        return nw ? (cta_major ? forward_kernel<T, L, H, true, true> : forward_kernel<T, L, H, true, false>)
+                  : (cta_major ? forward_kernel<T, L, H, false, true> : forward_kernel<T, L, H, false, false>);
+      }
+    };
+    auto kern = lane ? pick(std::true_type{}, std::false_type{}) : pick(std::false_type{}, std::false_type{});
     if constexpr (std::is_same<T, __half>::value)
-      if (h8) kern = nw ? forward_kernel<T, false, true, true> : forward_kernel<T, false, true, false>;
+      if (h8) kern = pick(std::false_type{}, std::true_type{});
     const size_t smem = size_t(F.max_box) * (lane ? 2 * sizeof(float) : sizeof(float4));
     allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     KernelTimer timer(RK_KERNEL_FORWARD, st);
