@@ -132,6 +132,11 @@ int rk_plan_info_get(const rk_plan* plan, rk_plan_info* info);
 int rk_plan_prepare(rk_plan* plan, uint64_t* hash);
 
 /* ------------------------------------------------------------- projector */
+/* Any batch >= 1: beyond 262,140 images (65,535 packed groups, one launch's
+ * grid limit) the device calls run consecutive sub-batches, bit-identical per
+ * image (rk_forward, rk_backproject, rk_filter_sinogram, rk_fbp and the *_host
+ * calls); the solvers and ADMM keep whole-batch state and return
+ * RK_ERR_VALIDATION above that batch. */
 /* image: batch x s x s (dtype) -> sino: batch x n_angles x det_count (dtype). */
 int rk_forward(rk_plan* plan, int dtype, const void* d_image, int64_t batch, void* d_sino, void* stream);
 /* sino: batch x n_angles x det_count -> image: batch x s x s. */
