@@ -420,6 +420,47 @@ def test_backprojector_thread_shapes_equal_bitwise(rk, oracle, cuda, tmp_path):
         assert np.isfinite(res["1"][name]).all()
 
 
+_ORDER_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+import paper_2009_14788_b200 as rk
+x = np.load({src!r})
+out = {{}}
+for name, g in [("par", rk.make_parallel(96, rk.angles_linspace(0.0, np.pi, 70), 131, 0.8)),
+                ("fan", rk.make_fanbeam(96, rk.angles_linspace(0.0, 2 * np.pi, 40), 150.0)),
+                ("coarse", rk.make_fanbeam(128, rk.angles_linspace(0.0, 2 * np.pi, 40), 128.0, det_count=16))]:
+    for dt in ("float32", "float16"):
+        xx = torch.from_numpy(np.ascontiguousarray(x[:, :g.image_size, :g.image_size]).astype(dt)).cuda()
+        out[name + dt] = rk.forward(g, xx).cpu().numpy()
+np.savez({dst!r}, **out)
+"""
+
+
+def test_forward_launch_orders_equal_bitwise(rk, oracle, cuda, tmp_path):
+    """The forward's CTA-major grid for few packed groups (kernels.cu launch_forward, CM) and
+    the group-major grid (RK_FWD_CTA_MAJOR_GROUPS=0) run the same CTAs: 13 images (four
+    float4 groups, two half8 groups), parallel / fan / narrow-warp schedules, identical bits."""
+    import os
+    import subprocess
+    import sys
+
+    src = str(tmp_path / "x.npy")
+    np.save(src, np.random.default_rng(31).uniform(0.0, 1.0, (13, 128, 128)).astype(np.float32))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("8", "0"):
+        dst = str(tmp_path / f"f{flag}.npz")
+        env = dict(os.environ, RK_FWD_CTA_MAJOR_GROUPS=flag)
+        script = _ORDER_SCRIPT.format(root=root, src=src, dst=dst)
+        r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(dst)
+    for k in res["8"].files:
+        assert np.array_equal(res["8"][k], res["0"][k]), k
+
+
 @pytest.mark.parametrize("name,mk", [
     ("fan-128-det16", lambda rk: fan(rk, 128, 40, 128.0, det_count=16)),      # spacing 16: narrow-warp tiers
     ("fan-96-det12", lambda rk: fan(rk, 96, 24, 96.0, det_count=12)),
