@@ -24,8 +24,15 @@ from .rng import Rng
 _FUSED = True  # fused device solvers of the C ABI (set False to run the generic torch loop)
 
 
-def _fused_ok(op: LinearOperator) -> bool:
-    return _FUSED and op.geometry is not None and A.torch is not None and A.torch.cuda.is_available()
+# the fused device solvers keep whole-batch packed state in one launch (65,535 packed
+# groups of four images); larger batches take the operator path, whose forward /
+# backprojection calls run sub-batches (capi.cpp for_sub_batches)
+_FUSED_MAX_BATCH = 65535 * 4
+
+
+def _fused_ok(op: LinearOperator, batch: int = 1) -> bool:
+    return (_FUSED and op.geometry is not None and A.torch is not None and A.torch.cuda.is_available()
+            and batch <= _FUSED_MAX_BATCH)
 
 
 def estimate_alpha(op: LinearOperator, iterations: int = 20, seed: int = 0) -> float:
@@ -67,7 +74,7 @@ def landweber(op: LinearOperator, y, guess, alpha: float, iterations: int):
         raise ValidationError("landweber iteration count must be >= 0")
     if y.shape[0] != guess.shape[0]:
         raise ValidationError(f"landweber: y batch {y.shape[0]} does not match guess batch {guess.shape[0]}")
-    if _fused_ok(op) and A.is_cuda(y) and A.is_cuda(guess) and guess.dtype != A.torch.float64:
+    if _fused_ok(op, guess.shape[0]) and A.is_cuda(y) and A.is_cuda(guess) and guess.dtype != A.torch.float64:
         return _landweber_fused(op, y, guess, alpha, iterations)
     torch = _torch()
     host = not A.is_torch(guess)
@@ -154,7 +161,7 @@ def cg(apply, guess, b, max_iter: int, tolerance: float = 0.0):
 
 def cgne(op: LinearOperator, guess, y, max_iter: int, tolerance: float = 0.0):
     """solvers.cpp:162-166: CG on the normal equations A'A x = A'y."""
-    if _fused_ok(op) and A.is_cuda(y) and A.is_cuda(guess) and guess.dtype != A.torch.float64:
+    if _fused_ok(op, guess.shape[0]) and A.is_cuda(y) and A.is_cuda(guess) and guess.dtype != A.torch.float64:
         torch = _torch()
         plan = get_plan(op.geometry, op.options, guess.device.index or 0)
         y = y.contiguous().to(guess.dtype)

@@ -212,6 +212,24 @@ def test_landweber_fused_equals_generic(rk, oracle, cuda):
     assert rel_l2(host(rk.cgne(op, torch.zeros_like(x), y, 6)), host(cg_generic)) <= 1e-5
 
 
+def test_solvers_beyond_one_launch(rk, cuda):
+    """262,141 images: more than the fused solvers' one-launch state (65,535 packed groups), so
+    Landweber and CGNE take the operator path (sub-batched projector calls); elements on both
+    sides of the launch boundary equal their single-image (fused) runs — bitwise for Landweber
+    (solvers.cpp:130-145), within fp32 CG rounding for CGNE."""
+    g = rk.make_parallel(4, [0.3, 1.1, 2.0], 5)
+    op = rk.projector_operator(g)
+    B = 65535 * 4 + 1
+    x = dev(np.random.default_rng(9).uniform(0.0, 1.0, (B, 4, 4)).astype(np.float32), cuda)
+    y = rk.forward(g, x)
+    z = torch.zeros_like(x)
+    lw = rk.landweber(op, y, z, 0.05, 3)
+    ne = rk.cgne(op, z, y, 3)
+    for i in (0, 65535 * 4 - 1, 65535 * 4):
+        assert torch.equal(lw[i:i + 1], rk.landweber(op, y[i:i + 1], z[i:i + 1], 0.05, 3))
+        assert rel_l2(host(ne[i:i + 1]), host(rk.cgne(op, z[i:i + 1], y[i:i + 1], 3))) <= 1e-5
+
+
 def test_solvers_batch_invariant(rk, oracle, cuda):
     """test_solvers.cpp:267-290: batched solver runs equal single-element runs bitwise."""
     g = rk.make_parallel(32, rk.angles_linspace(0.0, np.pi, 30))
