@@ -370,25 +370,35 @@ def main():
     stats = _lib.RkKernelStats()
     _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
 
-    clocks = ClockSampler(gpu)
-    clocks.start()
-    time.sleep(0.3)
-    _lib.check(_lib.lib.rk_profiling_enable(1))
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)  # L2 flush between timed steps (outside the events)
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-    torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
-    _lib.check(_lib.lib.rk_profiling_enable(0))
-    _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
-    clk = clocks.stop()
+    # a timed region that saw a hardware / thermal slowdown is measured once more (the
+    # contract rejects such a run); the decision is collective so every rank repeats it
+    remeasured = False
+    for attempt in range(2):
+        clocks = ClockSampler(gpu)
+        clocks.start()
+        time.sleep(0.3)
+        _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))  # reset the per-kind counters
+        _lib.check(_lib.lib.rk_profiling_enable(1))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        _lib.check(_lib.lib.rk_profiling_enable(0))
+        _lib.check(_lib.lib.rk_profiling_read(ctypes_ref(stats), 1))
+        clk = clocks.stop()
+        bad = bool(set(clk.get("reasons", [])) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"})
+        if attempt == 1 or max_over_ranks(1.0 if bad else 0.0) == 0.0:
+            break
+        remeasured = True
+    clk["remeasured"] = remeasured
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
