@@ -497,6 +497,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 constexpr int kTile = 32;
 constexpr int kBpHPWindow = 128;  // staged cells above which kf leaves the fp32-exact range (kBpParHP / kBpFan64)
 constexpr int kMaxBpChunk = 32;  // angles per staging pass (one constants record per thread of the first warp)
+// LANE stages 4-byte cells, so the same shared memory holds four times the angles: fewer
+// passes and barriers per tile (the batch-1 kernel's largest stall, ncu r2h)
+constexpr int kMaxBpChunkLane = 128;
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 
@@ -535,10 +538,12 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   // kernels keep the window-start origin — their tolerance is 1e-3 and they are issue-bound)
   constexpr bool kCentred = (KIND == kBpParallel || KIND == kBpFan32) && !std::is_same<TOut, __half>::value;
   const int wc = kCentred ? window >> 1 : 0;
-  const int chunk = min(kMaxBpChunk, cells / window);
+  // cells: staged window cells per pass (LANE: 4-byte cells, launch_backproject)
+  constexpr int kCap = LANE ? kMaxBpChunkLane : kMaxBpChunk;
+  const int chunk = min(kCap, cells / window);
   Cell* win = smem;                                                    // chunk * window <= cells
-  Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kMaxBpChunk records
-  int* ws_s = reinterpret_cast<int*>(cst + kMaxBpChunk);               // kMaxBpChunk window starts
+  Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kCap records
+  int* ws_s = reinterpret_cast<int*>(cst + kCap);                      // kCap window starts
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kTile + tx;
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile;
@@ -984,7 +989,15 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
                      : kind == kBpFan32  ? sizeof(Fan32Const)
                                          : sizeof(FanConst);
   const int cells = narrow ? p.bp_cells_narrow : p.bp_cells;
-  const size_t smem = size_t(cells) * sizeof(float4) + size_t(kMaxBpChunk) * (rec + sizeof(int));
+  // LANE: the same bytes as 4-byte cells, up to kMaxBpChunkLane angles per pass (RK_BP_LANE_WIDE=0: as
+  // many angles as the float4 kernels)
+  static const bool lane_wide = [] {
+    const char* e = std::getenv("RK_BP_LANE_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  const int cells_arg = lane && lane_wide ? 4 * cells : cells;
+  const size_t smem =
+      size_t(cells) * sizeof(float4) + size_t(lane ? kMaxBpChunkLane : kMaxBpChunk) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     // the kernel variant for one kind: single-lane (batch 1), half8, WIDE (one group), NARROW or 256 x 4
@@ -1006,7 +1019,7 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
     KernelTimer timer(RK_KERNEL_BACKPROJECT, st);
     kern<<<grid, block, smem, st>>>(packed_sino, int(p.s), int(p.na), int(p.nd), p.g.det_spacing,
                                     p.g.source_distance, p.g.det_distance, p.trig.as<double2>(),
-                                    p.bp_tile_window.as<int>(), cells, batch, static_cast<T*>(image), epi);
+                                    p.bp_tile_window.as<int>(), cells_arg, batch, static_cast<T*>(image), epi);
   });
   RK_CUDA(cudaGetLastError());
 }
