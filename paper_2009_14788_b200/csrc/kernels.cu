@@ -500,6 +500,9 @@ constexpr int kMaxBpChunk = 32;  // angles per staging pass (one constants recor
 // LANE stages 4-byte cells, so the same shared memory holds four times the angles: fewer
 // passes and barriers per tile (the batch-1 kernel's largest stall, ncu r2h)
 constexpr int kMaxBpChunkLane = 128;
+// H8 (two CTAs per SM of 512 threads): a window slab up to four times the plan's, as many
+// as two CTAs per SM still fit (launch_backproject), up to 128 angles per pass
+constexpr int kMaxBpChunkH8 = 128;
 constexpr int kRowsPerThread = 4;
 constexpr int kBpThreads = kTile * (kTile / kRowsPerThread);  // 256
 
@@ -539,7 +542,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   constexpr bool kCentred = (KIND == kBpParallel || KIND == kBpFan32) && !std::is_same<TOut, __half>::value;
   const int wc = kCentred ? window >> 1 : 0;
   // cells: staged window cells per pass (LANE: 4-byte cells, launch_backproject)
-  constexpr int kCap = LANE ? kMaxBpChunkLane : kMaxBpChunk;
+  constexpr int kCap = LANE ? kMaxBpChunkLane : (H8 || WIDE) ? kMaxBpChunkH8 : kMaxBpChunk;
   const int chunk = min(kCap, cells / window);
   Cell* win = smem;                                                    // chunk * window <= cells
   Const* cst = reinterpret_cast<Const*>(smem_raw + (LANE ? (cells + 3) / 4 : cells));  // kCap records
@@ -584,14 +587,14 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
   // Packed cells (float4 / half8) are staged by TMA bulk copies: one per angle
   // (the in-detector part of its window, a contiguous run of 16-byte cells),
   // issued by the thread that derived the window, completing on an mbarrier
-  // that warp 0's 32 lanes arrive on each pass; the out-of-detector cells are
+  // that threads 0 .. kCap-1 arrive on each pass; the out-of-detector cells are
   // zero-filled by the CTA.  This keeps the staging off the LSU (r1 loaded
   // the cells through L1 into registers and stored them).  LANE (lane 0 of
   // each cell) still stages through registers.
   __shared__ unsigned long long win_bar;
   if constexpr (!LANE) {
     if (tid == 0) {
-      mbar_init(&win_bar, 32);
+      mbar_init(&win_bar, min(kCap, NT));  // one arrival per thread tid < kCap each pass
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(NARROW ? 128 : (LANE || H8 || WIDE) ? 512 : kB
         if (bytes)
           tma_bulk_g2s(win + tid * window + (k0 - ws), sg + int64_t(a0 + tid) * nd + k0, bytes, &win_bar);
       }
-    } else if (!LANE && tid < 32) {
+    } else if (!LANE && tid < kCap) {
       mbar_arrive(&win_bar);
     }
     __syncthreads();
@@ -995,9 +998,23 @@ void launch_backproject(const Plan& p, const float4* packed_sino, int64_t batch,
     const char* e = std::getenv("RK_BP_LANE_WIDE");
     return !(e && e[0] == '0');
   }();
-  const int cells_arg = lane && lane_wide ? 4 * cells : cells;
-  const size_t smem =
-      size_t(cells) * sizeof(float4) + size_t(lane ? kMaxBpChunkLane : kMaxBpChunk) * (rec + sizeof(int));
+  static const bool wide_slab = [] {
+    const char* e = std::getenv("RK_BP_WIDE_SLAB");
+    return !(e && e[0] == '0');
+  }();
+  const int cap = lane ? kMaxBpChunkLane : (h8 || wide) ? kMaxBpChunkH8 : kMaxBpChunk;
+  // H8 / WIDE (512 threads, two CTAs per SM): the widest slab (4x, 2x the plan's) with which
+  // two CTAs still fit an SM's 228 KB (1 KB runtime reserve each): cfg2 windows take 4x
+  // (128 angles per pass), cfg3's 2x
+  int slab_factor = 1;
+  if ((h8 || wide) && wide_slab)
+    for (int f : {4, 2})
+      if (2 * (size_t(f) * cells * sizeof(float4) + size_t(cap) * (rec + sizeof(int)) + 1024 + 64) <= 233472) {
+        slab_factor = f;
+        break;
+      }
+  const int cells_arg = lane && lane_wide ? 4 * cells : (h8 || wide) ? slab_factor * cells : cells;
+  const size_t smem = size_t(lane ? cells : cells_arg) * sizeof(float4) + size_t(cap) * (rec + sizeof(int));
   dispatch_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     // the kernel variant for one kind: single-lane (batch 1), half8, WIDE (one group), NARROW or 256 x 4
