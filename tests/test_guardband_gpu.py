@@ -9,7 +9,7 @@ filled with a sentinel.
   bitwise with the plain call on a standalone tensor).
 
 Covers the forward / backprojection kernels of both beam types (single-lane
-batch 1, odd batches, the 512 tiers of configs 2 and 3), fp32 and fp16
+batch 1, partial lane groups, the group-major launch order beyond 8 groups, the 512 tiers of configs 2 and 3), fp32 and fp16
 storage, the ramp filter and the fused FBP.  Reference contract: outputs are
 exactly (B, n_angles, det_count) / (B, s, s) (projector.cpp:228-274,
 sino_filter.cpp:98-136).
@@ -77,7 +77,7 @@ def test_projectors_stay_in_bounds(rk, cuda, kind, s, na, kw, dtype):
 
     g = _geom(rk, kind, s, na, **kw)
     plan = get_plan(g, None, cuda.index or 0)
-    batches = (1, 3) if s >= 512 else (1, 3, 8)
+    batches = (1, 3, 9) if s >= 512 else (1, 3, 8, 37)  # single-lane, partial group, > 8 packed groups
     gen = torch.Generator(device="cpu").manual_seed(s * 1000 + na)
     for B in batches:
         img = torch.rand((B, s, s), generator=gen).to(dtype).to(cuda)
